@@ -1,0 +1,123 @@
+/*
+ * tir_b200.h — C-ABI of the B200 (sm_100a) tensorized-operator library.
+ *
+ * This is the drop-in boundary for the reference's intrinsic dispatch path:
+ *
+ *   tir::run → Interp::dispatch_call → HostKernel(std::vector<TensorView>&)
+ *   (/root/reference/proj/src/interp.cc:360-383, include/tir/interp.h:120)
+ *
+ * A HostKernel registered on tir::ExecContext (interp.cc:147-152) receives the
+ * operand views [writes[0], reads...] (interp.cc:371-373) and must compute the
+ * intrinsic's semantics *accumulating* into the output window (blockize moves
+ * `init` to the outer block, schedule_block.cc:570-603; the reference's own
+ * intrinsic test reads C first, tests/test_interp.cc:186). The C++ adapter in
+ * paper_2207_04296_b200/adapter/ packs the views and calls the entry points
+ * below; nothing here uses torch or C++ types.
+ *
+ * Operand conventions (following tests/testing/workloads.h):
+ *   GMM  A[M,K] fp16 row-major, B[K,N] fp16 row-major (N contiguous, workloads.h:45-51),
+ *        C[M,N] fp32 (or fp16) row-major.  C (+)= A·B, fp32 accumulation.
+ *   CONV X[N,(D,)(H,)W,CI] fp16 (NLC / NHWC / NDHWC, workloads.h:93-99),
+ *        W[(KD,)(KH,)KW,CI/G,CO] fp16 (HWIO-style), Y[N,(OD,)(OH,)OW,CO].
+ *        Covers C1D, C2D, C3D, DIL (dilation), GRP (groups), T2D (transposed,
+ *        gather form), and DEP (groups == CI == CO, CI/G == 1: W is [KH,KW,C],
+ *        workloads.h:132-137).
+ *
+ * All entry points are thread-safe given distinct streams, never throw, and
+ * return a status code; tir_b200_last_error() returns a thread-local message.
+ */
+#ifndef TIR_B200_H_
+#define TIR_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The adapter maps them onto tir::Error kinds (ir.h:33-48). */
+#define TIR_B200_OK 0
+#define TIR_B200_ERR_VALUE 1       /* bad argument / inexact fp16 input -> "ValueError"    */
+#define TIR_B200_ERR_UNSUPPORTED 2 /* legal op the kernels do not cover -> "UnsupportedShape" */
+#define TIR_B200_ERR_CUDA 3        /* CUDA runtime / driver failure    -> "CudaError"       */
+
+/* Operator tags (the paper's single-op suite). Informational for GMM..T2D; DEP
+ * selects the CUDA-core depthwise kernel. */
+typedef enum {
+  TIR_B200_GMM = 0,
+  TIR_B200_C1D = 1,
+  TIR_B200_C2D = 2,
+  TIR_B200_C3D = 3,
+  TIR_B200_DIL = 4,
+  TIR_B200_GRP = 5,
+  TIR_B200_T2D = 6,
+  TIR_B200_DEP = 7
+} tir_b200_op;
+
+/* Convolution geometry. Spatial dims are (D, H, W), outermost first; unused
+ * leading dims are 1 (C1D: D = H = 1, C2D: D = 1). Output extents follow
+ *   forward:    O = (I + 2p - d(K-1) - 1) / s + 1
+ *   transposed: O = (I - 1) s - 2p + d(K-1) + 1        (T2D, gather form)     */
+typedef struct {
+  int32_t op;         /* tir_b200_op */
+  int32_t transposed; /* 1: T2D gather form, out[o] += in[(o+p-k d)/s] w[k] when divisible */
+  int64_t n;
+  int64_t in_d, in_h, in_w;
+  int64_t ci, co;
+  int64_t k_d, k_h, k_w;
+  int64_t s_d, s_h, s_w;
+  int64_t p_d, p_h, p_w;
+  int64_t d_d, d_h, d_w; /* dilation */
+  int64_t groups;
+} tir_b200_conv_desc;
+
+/* Library / device facts. */
+int tir_b200_version(void);
+const char* tir_b200_last_error(void);
+/* Number of kernel launches issued by this thread since the last reset
+ * (bench.py's gpu_launches evidence). */
+int64_t tir_b200_launch_count(void);
+void tir_b200_reset_launch_count(void);
+
+/* Output extents (OD, OH, OW) for a descriptor; validates it. */
+int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]);
+
+/* ---- device-pointer entry points (asynchronous on `stream`, a cudaStream_t) ----
+ * accumulate = 1: Y = Yin + op(X, W) (Yin may alias Y); 0: Y = op(X, W).
+ * out_f16 = 1: Y is fp16 (round-to-nearest of the fp32 result); else fp32.
+ * Yin, when used, is always fp32. */
+int tir_b200_gmm(const uint16_t* A, const uint16_t* B, const float* Cin, void* C,
+                 int64_t M, int64_t N, int64_t K, int accumulate, int out_f16, void* stream);
+
+int tir_b200_conv(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                  const float* Yin, void* Y, int accumulate, int out_f16, void* stream);
+
+/* ---- host-buffer entry points (synchronous; H2D, compute, D2H) ----
+ * These are what the reference-side HostKernel adapter calls: operands live in
+ * host memory (the interpreter's TensorValues hold fp16 values as f32, ir.cc:36-47),
+ * so inputs are passed as f32 and converted to fp16 on the device; a value that
+ * is not exactly representable in fp16 is rejected with TIR_B200_ERR_VALUE.
+ * C/Y is read (accumulate = 1) and written as f32. Device buffers and pinned
+ * staging are cached per thread. */
+int tir_b200_gmm_host_f32(const float* A, const float* B, float* C, int64_t M, int64_t N,
+                          int64_t K, int accumulate);
+
+int tir_b200_conv_host_f32(const tir_b200_conv_desc* desc, const float* X, const float* W,
+                           float* Y, int accumulate);
+
+/* Same, but with fp16 host inputs (pinned or pageable), the e2e benchmark path. */
+int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M, int64_t N,
+                      int64_t K, int accumulate);
+
+int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                       float* Y, int accumulate);
+
+/* Frees the calling thread's cached device/pinned buffers. */
+void tir_b200_release_host_cache(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TIR_B200_H_ */

@@ -1,0 +1,83 @@
+// prep.cuh — bit-exact layout / conversion steps around the contraction kernel.
+//
+//  * pad_channels: X[..., C] -> Xp[..., Cp] with zero channels (Cp = C rounded up
+//    to 8). TMA needs a 16-byte pixel pitch; the CI = 3 first layers (C3D, DIL,
+//    SURVEY §7 "hard parts") go through this. Zero channels meet zero weight
+//    rows, so every real product and partial sum is unchanged.
+//  * pad_weight_rows: W[taps, C, CO] -> Wp[taps, Cp, CO], zero rows.
+//  * f32_to_f16_exact: the host-buffer entry points receive the interpreter's
+//    f32 storage of F16 values (ir.cc:36-47); convert with RN and flag any
+//    value that does not survive the round trip (rejected as ValueError).
+#pragma once
+
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace tb {
+
+__global__ void pad_channels_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
+                                    int64_t pixels, int32_t c, int32_t cp) {
+  const int64_t total = pixels * cp;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t pix = i / cp;
+    const int32_t ch = static_cast<int32_t>(i - pix * cp);
+    y[i] = ch < c ? x[pix * c + ch] : static_cast<uint16_t>(0);
+  }
+}
+
+__global__ void pad_weight_rows_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ y,
+                                       int64_t taps, int32_t c, int32_t cp, int32_t co) {
+  const int64_t total = taps * cp * co;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t col = i % co;
+    const int64_t row = i / co;
+    const int64_t tap = row / cp;
+    const int32_t ch = static_cast<int32_t>(row - tap * cp);
+    y[i] = ch < c ? w[(tap * c + ch) * co + col] : static_cast<uint16_t>(0);
+  }
+}
+
+__global__ void f32_to_f16_exact_kernel(const float* __restrict__ x, uint16_t* __restrict__ y,
+                                        int64_t n, int* flag) {
+  bool bad = false;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const float v = x[i];
+    const __half h = __float2half_rn(v);
+    const float back = __half2float(h);
+    // NaN never compares equal; the reference's f16 tag stores finite values.
+    if (!(back == v)) bad = true;
+    y[i] = __half_as_ushort(h);
+  }
+  if (bad) atomicExch(flag, 1);
+}
+
+inline int grid_for(int64_t n) {
+  int64_t b = (n + 255) / 256;
+  return static_cast<int>(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
+}
+
+inline int launch_pad_channels(const uint16_t* x, uint16_t* y, int64_t pixels, int64_t c,
+                               int64_t cp, cudaStream_t st) {
+  pad_channels_kernel<<<grid_for(pixels * cp), 256, 0, st>>>(x, y, pixels, static_cast<int32_t>(c),
+                                                             static_cast<int32_t>(cp));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+inline int launch_pad_weight_rows(const uint16_t* w, uint16_t* y, int64_t taps, int64_t c,
+                                  int64_t cp, int64_t co, cudaStream_t st) {
+  pad_weight_rows_kernel<<<grid_for(taps * cp * co), 256, 0, st>>>(
+      w, y, taps, static_cast<int32_t>(c), static_cast<int32_t>(cp), static_cast<int32_t>(co));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+inline int launch_f32_to_f16_exact(const float* x, uint16_t* y, int64_t n, int* flag,
+                                   cudaStream_t st) {
+  f32_to_f16_exact_kernel<<<grid_for(n), 256, 0, st>>>(x, y, n, flag);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+}  // namespace tb

@@ -1,0 +1,796 @@
+// tir_b200.cu — the C-ABI (include/tir_b200.h): operator planning, TMA
+// descriptor encoding, kernel launches, host-buffer entry points.
+//
+// Each entry point replaces the body of one reference HostKernel
+// (/root/reference/proj/include/tir/interp.h:120): the adapter
+// (paper_2207_04296_b200/adapter/) turns the views of a tensorized block
+// (src/interp.cc:371-373) into one of these calls.
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/tir_b200.h"
+#include "dep.cuh"
+#include "igemm.cuh"
+#include "prep.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess)                                                               \
+      return set_err(TIR_B200_ERR_CUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), \
+                     __FILE__, __LINE__);                                                \
+  } while (0)
+
+// ------------------------------------------------------------------ driver API
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                    const cuuint64_t*, const cuuint64_t*, const int*, const int*,
+                                    cuuint32_t, cuuint32_t, const cuuint32_t*,
+                                    CUtensorMapInterleave, CUtensorMapSwizzle,
+                                    CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct Driver {
+  EncodeTiledFn tiled = nullptr;
+  EncodeIm2colFn im2col = nullptr;
+  int version = 0;
+};
+
+const Driver* driver() {
+  static Driver d;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      d.tiled = reinterpret_cast<EncodeTiledFn>(fn);
+    fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess && q == cudaDriverEntryPointSuccess)
+      d.im2col = reinterpret_cast<EncodeIm2colFn>(fn);
+    cudaDriverGetVersion(&d.version);
+  });
+  return &d;
+}
+
+struct DeviceInfo {
+  int sms = 148;
+  int smem_optin = 227 * 1024;
+};
+
+DeviceInfo device_info() {
+  static std::mutex mu;
+  static DeviceInfo cache[64];
+  static bool have[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (dev >= 0 && dev < 64 && !have[dev]) {
+    cudaDeviceGetAttribute(&cache[dev].sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&cache[dev].smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    have[dev] = true;
+  }
+  return cache[(dev >= 0 && dev < 64) ? dev : 0];
+}
+
+CUtensorMapSwizzle swizzle_for(int row_bytes) {
+  switch (row_bytes) {
+    case 128: return CU_TENSOR_MAP_SWIZZLE_128B;
+    case 64: return CU_TENSOR_MAP_SWIZZLE_64B;
+    case 32: return CU_TENSOR_MAP_SWIZZLE_32B;
+    default: return CU_TENSOR_MAP_SWIZZLE_NONE;
+  }
+}
+
+// Row-major [rows, cols] fp16 matrix, box {box_cols, box_rows}.
+int encode_2d(CUtensorMap* m, const void* ptr, int64_t rows, int64_t cols, int box_cols,
+              int box_rows) {
+  const Driver* d = driver();
+  if (!d->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(cols) * 2};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(box_cols), static_cast<cuuint32_t>(box_rows)};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = d->tiled(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(ptr), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        swizzle_for(box_cols * 2), CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld box=%dx%d",
+                   static_cast<int>(r), static_cast<long long>(rows), static_cast<long long>(cols),
+                   box_cols, box_rows);
+  return TIR_B200_OK;
+}
+
+// ------------------------------------------------------------------ geometry
+
+struct Geo {
+  int64_t n, in[3], ci, co, k[3], s[3], p[3], d[3], g, out[3];  // [0]=D,[1]=H,[2]=W
+  bool transposed;
+};
+
+int make_geo(const tir_b200_conv_desc* desc, Geo* g) {
+  if (!desc) return set_err(TIR_B200_ERR_VALUE, "null descriptor");
+  g->n = desc->n;
+  g->in[0] = desc->in_d; g->in[1] = desc->in_h; g->in[2] = desc->in_w;
+  g->ci = desc->ci; g->co = desc->co;
+  g->k[0] = desc->k_d; g->k[1] = desc->k_h; g->k[2] = desc->k_w;
+  g->s[0] = desc->s_d; g->s[1] = desc->s_h; g->s[2] = desc->s_w;
+  g->p[0] = desc->p_d; g->p[1] = desc->p_h; g->p[2] = desc->p_w;
+  g->d[0] = desc->d_d; g->d[1] = desc->d_h; g->d[2] = desc->d_w;
+  g->g = desc->groups;
+  g->transposed = desc->transposed != 0;
+  if (g->n < 1 || g->ci < 1 || g->co < 1 || g->g < 1)
+    return set_err(TIR_B200_ERR_VALUE, "conv: n, ci, co, groups must be >= 1");
+  if (g->ci % g->g || g->co % g->g)
+    return set_err(TIR_B200_ERR_VALUE, "conv: groups must divide ci and co");
+  for (int i = 0; i < 3; ++i) {
+    if (g->in[i] < 1 || g->k[i] < 1 || g->s[i] < 1 || g->p[i] < 0 || g->d[i] < 1)
+      return set_err(TIR_B200_ERR_VALUE, "conv: bad extents/stride/padding/dilation");
+    if (g->transposed) {
+      g->out[i] = (g->in[i] - 1) * g->s[i] - 2 * g->p[i] + g->d[i] * (g->k[i] - 1) + 1;
+    } else {
+      int64_t span = g->in[i] + 2 * g->p[i] - g->d[i] * (g->k[i] - 1) - 1;
+      if (span < 0) return set_err(TIR_B200_ERR_VALUE, "conv: kernel larger than padded input");
+      g->out[i] = span / g->s[i] + 1;
+    }
+    if (g->out[i] < 1) return set_err(TIR_B200_ERR_VALUE, "conv: empty output");
+  }
+  const int64_t in_elems = g->n * g->in[0] * g->in[1] * g->in[2] * g->ci;
+  const int64_t out_elems = g->n * g->out[0] * g->out[1] * g->out[2] * g->co;
+  if (in_elems >= (1ll << 31) * 8 || out_elems >= (1ll << 31) * 8)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: tensor too large");
+  return TIR_B200_OK;
+}
+
+bool is_depthwise(const Geo& g) { return g.g == g.ci && g.ci == g.co && !g.transposed; }
+
+// ------------------------------------------------------------------ workspace
+
+struct Workspace {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int dev = -1;
+};
+thread_local Workspace t_ws;
+
+int workspace(size_t bytes, void** out) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (t_ws.dev != dev || t_ws.bytes < bytes) {
+    if (t_ws.ptr) {
+      int cur = dev;
+      cudaSetDevice(t_ws.dev);
+      cudaFree(t_ws.ptr);
+      cudaSetDevice(cur);
+    }
+    t_ws = Workspace{};
+    CUDA_TRY(cudaMalloc(&t_ws.ptr, bytes));
+    t_ws.bytes = bytes;
+    t_ws.dev = dev;
+  }
+  *out = t_ws.ptr;
+  return TIR_B200_OK;
+}
+
+// ------------------------------------------------------------------ igemm launch
+
+template <int BN>
+int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
+  using Cfg = tb::IgemmCfg<BN>;
+  const DeviceInfo di = device_info();
+  const int budget = di.smem_optin - 1024 - 256;
+  p.stages = std::min(8, budget / Cfg::kStageBytes);
+  if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
+  const size_t smem = Cfg::smem_bytes(p.stages);
+  CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  const int grid = std::min(p.total_tiles, di.sms);
+  tb::igemm_tc_kernel<BN><<<grid, tb::kThreads, smem, stream>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int launch_igemm(tb::IgemmParams& p, int bn, cudaStream_t stream) {
+  switch (bn) {
+    case 16: return launch_igemm_bn<16>(p, stream);
+    case 32: return launch_igemm_bn<32>(p, stream);
+    case 64: return launch_igemm_bn<64>(p, stream);
+    case 128: return launch_igemm_bn<128>(p, stream);
+    case 256: return launch_igemm_bn<256>(p, stream);
+  }
+  return set_err(TIR_B200_ERR_UNSUPPORTED, "no kernel for BN=%d", bn);
+}
+
+// Chooses the N tile: the whole (group) width when that still gives at least
+// one wave of tiles, else the narrowest power of two >= 16 that does.
+int choose_bn(int64_t cols, int64_t m_tiles, int64_t groups, int sms) {
+  int bn = 16;
+  while (bn < cols && bn < 256) bn *= 2;
+  while (bn > 16 && m_tiles * groups * ((cols + bn - 1) / bn) < sms) bn /= 2;
+  return bn;
+}
+
+void set_sub_identity(tb::SubProb& s) {
+  for (int i = 0; i < 3; ++i) {
+    s.a_lo[i] = 0; s.a_st[i] = 1; s.taps[i] = 1; s.a_dil[i] = 1;
+    s.w_base[i] = 0; s.w_step[i] = 1; s.o_st[i] = 1; s.o_b[i] = 0;
+  }
+}
+
+int finalize_tiles(tb::IgemmParams& p, int bn) {
+  p.tiles_n = static_cast<int32_t>((p.cog + bn - 1) / bn);
+  int64_t t = 0;
+  for (int i = 0; i < p.num_sub; ++i) {
+    tb::SubProb& s = p.sub[i];
+    s.tiles_m = (s.m_count + tb::kBM - 1) / tb::kBM;
+    s.tile_begin = static_cast<int32_t>(t);
+    t += static_cast<int64_t>(s.tiles_m) * p.groups * p.tiles_n;
+    const int pps = tb::kBK / p.a_box_ch;
+    s.num_stages = (s.num_pieces + pps - 1) / pps;
+  }
+  if (t >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "too many tiles");
+  p.total_tiles = static_cast<int32_t>(t);
+  return TIR_B200_OK;
+}
+
+// ------------------------------------------------------------------ GMM
+
+int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
+             int64_t N, int64_t K, int accumulate, int out_f16, cudaStream_t stream) {
+  if (M < 0 || N < 0 || K < 0) return set_err(TIR_B200_ERR_VALUE, "gmm: negative extent");
+  if (M == 0 || N == 0) return TIR_B200_OK;
+  if (K == 0) {  // C = Cin (or 0): nothing to contract
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm: K == 0");
+  }
+  if (!A || !B || !C || (accumulate && !Cin)) return set_err(TIR_B200_ERR_VALUE, "gmm: null operand");
+  if (K % 8 || N % 8)
+    return set_err(TIR_B200_ERR_UNSUPPORTED,
+                   "gmm: K and N must be multiples of 8 (16-byte TMA row pitch); got K=%lld N=%lld",
+                   static_cast<long long>(K), static_cast<long long>(N));
+  if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31))
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm: extent too large");
+  const DeviceInfo di = device_info();
+  tb::IgemmParams p;
+  std::memset(&p, 0, sizeof p);
+  const int bn = choose_bn(N, (M + tb::kBM - 1) / tb::kBM, 1, di.sms);
+  int rc = encode_2d(&p.tmA[0], A, M, K, 64, tb::kBM);
+  if (rc) return rc;
+  rc = encode_2d(&p.tmB, B, K, N, std::min(bn, 64), tb::kBK);
+  if (rc) return rc;
+  p.num_sub = 1;
+  tb::SubProb& s = p.sub[0];
+  set_sub_identity(s);
+  s.m_count = static_cast<int32_t>(M);
+  s.gx = static_cast<int32_t>(M);
+  s.gy = s.gz = 1;
+  s.num_pieces = static_cast<int32_t>((K + 63) / 64);
+  p.groups = 1;
+  p.a_mode = tb::A_TILED;
+  p.a_box_ch = 64;
+  p.cig = static_cast<int32_t>(K);
+  p.cb_per_tap = s.num_pieces;
+  p.b_contig = 1;
+  p.k_rows = static_cast<int32_t>(K);
+  p.w_kx = p.w_ky = 1;
+  p.cog = static_cast<int32_t>(N);
+  p.ldy = static_cast<int32_t>(N);
+  p.out_dims[0] = static_cast<int32_t>(M);
+  p.out_dims[1] = p.out_dims[2] = 1;
+  p.accumulate = accumulate;
+  p.out_f16 = out_f16;
+  p.Y = C;
+  p.Yin = Cin;
+  rc = finalize_tiles(p, bn);
+  if (rc) return rc;
+  return launch_igemm(p, bn, stream);
+}
+
+// ------------------------------------------------------------------ conv (tensor cores)
+
+int corner_limit(int rank) { return rank == 3 ? 32768 : rank == 4 ? 128 : 16; }
+int offset_limit(int rank) { return rank == 3 ? 65536 : rank == 4 ? 256 : 32; }
+
+// Im2col tensor map over X[N, (D,) (H,) W, C] (C contiguous).
+int encode_im2col(CUtensorMap* m, const void* X, const Geo& g, int64_t c_total, int rank,
+                  const int lower[3], const int upper[3], const int estride[3], int box_ch) {
+  const Driver* d = driver();
+  if (!d->im2col) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeIm2col unavailable");
+  // dims in TMA order: C, W, H, D, N (truncated to rank)
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t estr[5];
+  int lo[3], up[3];
+  const int nsp = rank - 2;  // spatial dims used: W (, H (, D))
+  dims[0] = static_cast<cuuint64_t>(c_total);
+  estr[0] = 1;
+  int64_t pitch = c_total * 2;
+  for (int i = 0; i < nsp; ++i) {  // i=0:W, 1:H, 2:D  -> Geo index 2-i
+    dims[1 + i] = static_cast<cuuint64_t>(g.in[2 - i]);
+    strides[i] = static_cast<cuuint64_t>(pitch);
+    pitch *= g.in[2 - i];
+    estr[1 + i] = static_cast<cuuint32_t>(estride[2 - i]);
+    lo[i] = lower[2 - i];
+    up[i] = upper[2 - i];
+  }
+  // dims of unused spatial extents (must be 1) fold into the batch pitch
+  for (int i = nsp; i < 3; ++i) pitch *= g.in[2 - i];
+  dims[rank - 1] = static_cast<cuuint64_t>(g.n);
+  strides[rank - 2] = static_cast<cuuint64_t>(pitch);
+  estr[rank - 1] = 1;
+  const int lim = corner_limit(rank);
+  for (int i = 0; i < nsp; ++i)
+    if (lo[i] < -lim || lo[i] >= lim || up[i] < -lim || up[i] >= lim)
+      return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: im2col corner out of range (%d, %d)", lo[i],
+                     up[i]);
+  CUresult r = d->im2col(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, static_cast<cuuint32_t>(rank),
+                         const_cast<void*>(X), dims, strides, lo, up,
+                         static_cast<cuuint32_t>(box_ch), static_cast<cuuint32_t>(tb::kBM), estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle_for(box_ch * 2),
+                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeIm2col failed (%d)", static_cast<int>(r));
+  // Same driver workaround CUTLASS applies to small im2col tensors (<= r580 drivers).
+  const int64_t bytes = g.n * g.in[0] * g.in[1] * g.in[2] * c_total * 2;
+  if (d->version <= 13010 && bytes < 131072) reinterpret_cast<uint64_t*>(m)[1] &= ~(1ull << 21);
+  return TIR_B200_OK;
+}
+
+int pick_box(int64_t cig) {
+  for (int b : {64, 32, 16, 8})
+    if (cig % b == 0) return b;
+  return 0;
+}
+
+int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,
+                 int accumulate, int out_f16, cudaStream_t stream) {
+  Geo g = g0;
+  const uint16_t* X = X0;
+  const uint16_t* W = W0;
+  int64_t cig = g.ci / g.g;
+  const int64_t cog = g.co / g.g;
+  const int64_t taps = g.k[0] * g.k[1] * g.k[2];
+  // Channel padding (a bit-exact layout step): TMA needs a 16-byte pixel pitch.
+  if (cig % 8) {
+    if (g.g != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: grouped conv needs CI/G %% 8 == 0");
+    const int64_t cip = (cig + 7) / 8 * 8;
+    const int64_t pix = g.n * g.in[0] * g.in[1] * g.in[2];
+    const size_t xbytes = static_cast<size_t>(pix * cip * 2);
+    const size_t wbytes = static_cast<size_t>(taps * cip * g.co * 2);
+    void* ws = nullptr;
+    int rc = workspace(xbytes + wbytes + 256, &ws);
+    if (rc) return rc;
+    uint16_t* Xp = static_cast<uint16_t*>(ws);
+    uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
+    rc = tb::launch_pad_channels(X, Xp, pix, cig, cip, stream);
+    if (rc) return set_err(TIR_B200_ERR_CUDA, "pad kernel launch failed");
+    ++g_launches;
+    rc = tb::launch_pad_weight_rows(W, Wp, taps, cig, cip, g.co, stream);
+    if (rc) return set_err(TIR_B200_ERR_CUDA, "pad kernel launch failed");
+    ++g_launches;
+    X = Xp;
+    W = Wp;
+    g.ci = cip;
+    cig = cip;
+  }
+  const int box = pick_box(cig);
+  if (!box) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: channels per group %lld", (long long)cig);
+  if (g.co % 8) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: CO must be a multiple of 8");
+  // Spatial rank of the TMA view.
+  int rank = 5;
+  if (g.in[0] == 1 && g.k[0] == 1 && g.p[0] == 0 && g.s[0] == 1) {
+    rank = (g.in[1] == 1 && g.k[1] == 1 && g.p[1] == 0 && g.s[1] == 1) ? 3 : 4;
+  }
+  const int nsp = rank - 2;
+  auto used = [&](int i) { return i >= 3 - nsp; };  // Geo index i (0=D,1=H,2=W)
+
+  const DeviceInfo di = device_info();
+  tb::IgemmParams p;
+  std::memset(&p, 0, sizeof p);
+  p.groups = static_cast<int32_t>(g.g);
+  p.a_mode = rank;
+  p.a_box_ch = box;
+  p.cig = static_cast<int32_t>(cig);
+  p.cb_per_tap = static_cast<int32_t>(cig / box);
+  p.k_rows = static_cast<int32_t>(taps * cig);
+  p.w_kx = static_cast<int32_t>(g.k[2]);
+  p.w_ky = static_cast<int32_t>(g.k[1]);
+  p.cog = static_cast<int32_t>(cog);
+  p.ldy = static_cast<int32_t>(g.co);
+  p.out_dims[0] = static_cast<int32_t>(g.out[2]);
+  p.out_dims[1] = static_cast<int32_t>(g.out[1]);
+  p.out_dims[2] = static_cast<int32_t>(g.out[0]);
+  p.accumulate = accumulate;
+  p.out_f16 = out_f16;
+  p.Y = Y;
+  p.Yin = Yin;
+
+  const int lim_off = offset_limit(rank);
+  if (!g.transposed) {
+    p.num_sub = 1;
+    tb::SubProb& s = p.sub[0];
+    set_sub_identity(s);
+    int lower[3], upper[3], estr[3];
+    for (int i = 0; i < 3; ++i) {
+      lower[i] = used(i) ? static_cast<int>(-g.p[i]) : 0;
+      upper[i] = used(i) ? static_cast<int>(g.p[i] - g.d[i] * (g.k[i] - 1)) : 0;
+      estr[i] = used(i) ? static_cast<int>(g.s[i]) : 1;
+      if (used(i) && (g.k[i] - 1) * g.d[i] >= lim_off)
+        return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: dilated kernel extent exceeds im2col offsets");
+      if (used(i) && g.s[i] > 8)
+        return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: stride > 8");
+    }
+    const int64_t M = g.n * g.out[0] * g.out[1] * g.out[2];
+    if (M >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: too many output pixels");
+    s.m_count = static_cast<int32_t>(M);
+    s.gx = static_cast<int32_t>(g.out[2]);
+    s.gy = static_cast<int32_t>(g.out[1]);
+    s.gz = static_cast<int32_t>(g.out[0]);
+    for (int i = 0; i < 3; ++i) {  // SubProb index 0=x(W),1=y(H),2=z(D) <- Geo 2-i
+      s.a_lo[i] = lower[2 - i];
+      s.a_st[i] = static_cast<int32_t>(g.s[2 - i]);
+      s.taps[i] = static_cast<int32_t>(g.k[2 - i]);
+      s.a_dil[i] = static_cast<int32_t>(g.d[2 - i]);
+    }
+    s.num_pieces = static_cast<int32_t>(taps * p.cb_per_tap);
+    p.b_contig = 1;
+    int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, box);
+    if (rc) return rc;
+    const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, di.sms);
+    rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK);
+    if (rc) return rc;
+    rc = finalize_tiles(p, bn);
+    if (rc) return rc;
+    return launch_igemm(p, bn, stream);
+  }
+
+  // Transposed (T2D): sub-pixel decomposition into prod(s) stride-1 convs, one
+  // per output parity class q: o = s*a + q, taps k = r0 + s*t (r0 = (q+p) mod s),
+  // input i = a + c - t (c = (q+p) div s). Flipping t makes each class a forward
+  // correlation with lower corner c - (T-1); the epilogue scatters rows to o.
+  if (g.g != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: groups must be 1");
+  for (int i = 0; i < 3; ++i)
+    if (g.d[i] != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: dilation must be 1");
+  const int nclass = static_cast<int>(g.s[0] * g.s[1] * g.s[2]);
+  if (nclass > tb::kMaxSub)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: %d sub-pixel classes (max %d)", nclass, tb::kMaxSub);
+  p.b_contig = 0;
+  int64_t m_max = 0;
+  int ns = 0;
+  for (int qd = 0; qd < g.s[0]; ++qd)
+    for (int qh = 0; qh < g.s[1]; ++qh)
+      for (int qw = 0; qw < g.s[2]; ++qw) {
+        const int q[3] = {qd, qh, qw};
+        int lower[3], upper[3], estr[3] = {1, 1, 1};
+        int T[3], A[3], base[3], step[3];
+        bool empty = false;
+        for (int i = 0; i < 3; ++i) {
+          const int64_t s_ = g.s[i], p_ = g.p[i], k_ = g.k[i];
+          const int64_t r0 = (q[i] + p_) % s_;
+          const int64_t c = (q[i] + p_) / s_;
+          T[i] = k_ > r0 ? static_cast<int>((k_ - r0 + s_ - 1) / s_) : 0;
+          A[i] = g.out[i] > q[i] ? static_cast<int>((g.out[i] - q[i] + s_ - 1) / s_) : 0;
+          if (T[i] == 0 || A[i] == 0) empty = true;
+          lower[i] = static_cast<int>(c - (T[i] - 1));
+          upper[i] = static_cast<int>(A[i] - g.in[i] + lower[i]);
+          base[i] = static_cast<int>(r0 + s_ * (T[i] - 1));
+          step[i] = static_cast<int>(-s_);
+          if (!used(i)) { lower[i] = upper[i] = 0; }
+        }
+        if (empty) {
+          if (A[0] && A[1] && A[2])
+            return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: kernel smaller than stride");
+          continue;
+        }
+        tb::SubProb& s = p.sub[ns];
+        set_sub_identity(s);
+        const int64_t M = g.n * static_cast<int64_t>(A[0]) * A[1] * A[2];
+        s.m_count = static_cast<int32_t>(M);
+        m_max = std::max(m_max, M);
+        s.gx = A[2];
+        s.gy = A[1];
+        s.gz = A[0];
+        for (int i = 0; i < 3; ++i) {
+          s.a_lo[i] = lower[2 - i];
+          s.a_st[i] = 1;
+          s.taps[i] = T[2 - i];
+          s.a_dil[i] = 1;
+          s.w_base[i] = base[2 - i];
+          s.w_step[i] = step[2 - i];
+          s.o_st[i] = static_cast<int32_t>(g.s[2 - i]);
+          s.o_b[i] = q[2 - i];
+        }
+        s.num_pieces = T[0] * T[1] * T[2] * p.cb_per_tap;
+        int rc = encode_im2col(&p.tmA[ns], X, g, g.ci, rank, lower, upper, estr, box);
+        if (rc) return rc;
+        ++ns;
+      }
+  p.num_sub = ns;
+  if (ns == 0) return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: no output classes");
+  const int bn = choose_bn(cog, (m_max + tb::kBM - 1) / tb::kBM * ns, 1, di.sms);
+  int rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), box);
+  if (rc) return rc;
+  rc = finalize_tiles(p, bn);
+  if (rc) return rc;
+  return launch_igemm(p, bn, stream);
+}
+
+// ------------------------------------------------------------------ DEP
+
+int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
+             int accumulate, int out_f16, cudaStream_t stream) {
+  if (g.in[0] != 1 || g.k[0] != 1)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: 2-D (NHWC) depthwise only");
+  tb::DepParams p;
+  p.X = reinterpret_cast<const __half*>(X);
+  p.W = reinterpret_cast<const __half*>(W);
+  p.Yin = Yin;
+  p.Y = Y;
+  p.n = static_cast<int32_t>(g.n);
+  p.ih = static_cast<int32_t>(g.in[1]);
+  p.iw = static_cast<int32_t>(g.in[2]);
+  p.c = static_cast<int32_t>(g.ci);
+  p.oh = static_cast<int32_t>(g.out[1]);
+  p.ow = static_cast<int32_t>(g.out[2]);
+  p.kh = static_cast<int32_t>(g.k[1]);
+  p.kw = static_cast<int32_t>(g.k[2]);
+  p.sh = static_cast<int32_t>(g.s[1]);
+  p.sw = static_cast<int32_t>(g.s[2]);
+  p.ph = static_cast<int32_t>(g.p[1]);
+  p.pw = static_cast<int32_t>(g.p[2]);
+  p.dh = static_cast<int32_t>(g.d[1]);
+  p.dw = static_cast<int32_t>(g.d[2]);
+  p.accumulate = accumulate;
+  p.out_f16 = out_f16;
+  const DeviceInfo di = device_info();
+  constexpr int R = 4;
+  const bool vec = (g.ci % 8 == 0) && (reinterpret_cast<uintptr_t>(X) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&
+                   (reinterpret_cast<uintptr_t>(Y) % 32 == 0);
+  const int v = vec ? 8 : 1;
+  const int64_t work = g.n * ((g.out[1] + R - 1) / R) * g.out[2] * (g.ci / v);
+  const int64_t blocks = std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(di.sms) * 16);
+  if (vec)
+    tb::dep_kernel<8, R><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
+  else
+    tb::dep_kernel<1, R><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+              const float* Yin, void* Y, int accumulate, int out_f16, cudaStream_t stream) {
+  Geo g;
+  int rc = make_geo(desc, &g);
+  if (rc) return rc;
+  if (!X || !W || !Y || (accumulate && !Yin)) return set_err(TIR_B200_ERR_VALUE, "conv: null operand");
+  // Depthwise (CI/G == 1) is not a dense contraction: CUDA-core kernel.
+  if (desc->op == TIR_B200_DEP || is_depthwise(g)) {
+    if (!is_depthwise(g)) return set_err(TIR_B200_ERR_VALUE, "DEP requires groups == ci == co");
+    return dep_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+  }
+  return conv_tc_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+}
+
+// ------------------------------------------------------------------ host-buffer paths
+
+struct HostCache {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  void* dbuf = nullptr;
+  size_t dbytes = 0;
+  int* dflag = nullptr;
+};
+thread_local HostCache t_host;
+
+int host_prepare(size_t bytes, char** base) {
+  int dev = 0;
+  CUDA_TRY(cudaGetDevice(&dev));
+  if (t_host.dev != dev) {
+    tir_b200_release_host_cache();
+    CUDA_TRY(cudaStreamCreateWithFlags(&t_host.stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&t_host.dflag), sizeof(int)));
+    t_host.dev = dev;
+  }
+  if (t_host.dbytes < bytes) {
+    if (t_host.dbuf) cudaFree(t_host.dbuf);
+    t_host.dbuf = nullptr;
+    t_host.dbytes = 0;
+    CUDA_TRY(cudaMalloc(&t_host.dbuf, bytes));
+    t_host.dbytes = bytes;
+  }
+  *base = static_cast<char*>(t_host.dbuf);
+  return TIR_B200_OK;
+}
+
+size_t align256(size_t b) { return (b + 255) / 256 * 256; }
+
+// H2D of f32 host values, then device RN conversion to fp16 with an exactness flag.
+int upload_f32_as_f16(const float* host, size_t n, float* dstage, uint16_t* d16, cudaStream_t st) {
+  CUDA_TRY(cudaMemcpyAsync(dstage, host, n * 4, cudaMemcpyHostToDevice, st));
+  if (tb::launch_f32_to_f16_exact(dstage, d16, static_cast<int64_t>(n), t_host.dflag, st))
+    return set_err(TIR_B200_ERR_CUDA, "convert kernel launch failed");
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+}  // namespace
+
+// ====================================================================== C-ABI
+
+extern "C" {
+
+int tir_b200_version(void) { return 1; }
+const char* tir_b200_last_error(void) { return g_err.c_str(); }
+int64_t tir_b200_launch_count(void) { return g_launches; }
+void tir_b200_reset_launch_count(void) { g_launches = 0; }
+
+int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]) {
+  Geo g;
+  int rc = make_geo(desc, &g);
+  if (rc) return rc;
+  for (int i = 0; i < 3; ++i) out_dhw[i] = g.out[i];
+  return TIR_B200_OK;
+}
+
+int tir_b200_gmm(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
+                 int64_t N, int64_t K, int accumulate, int out_f16, void* stream) {
+  return gmm_impl(A, B, Cin, C, M, N, K, accumulate, out_f16, static_cast<cudaStream_t>(stream));
+}
+
+int tir_b200_conv(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                  const float* Yin, void* Y, int accumulate, int out_f16, void* stream) {
+  return conv_impl(desc, X, W, Yin, Y, accumulate, out_f16, static_cast<cudaStream_t>(stream));
+}
+
+int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M, int64_t N,
+                      int64_t K, int accumulate) {
+  if (M < 0 || N < 0 || K < 0) return set_err(TIR_B200_ERR_VALUE, "gmm: negative extent");
+  const size_t a = align256(M * K * 2), b = align256(K * N * 2), c = align256(M * N * 4);
+  char* d = nullptr;
+  int rc = host_prepare(a + b + c, &d);
+  if (rc) return rc;
+  cudaStream_t st = t_host.stream;
+  CUDA_TRY(cudaMemcpyAsync(d, A, M * K * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d + a, B, K * N * 2, cudaMemcpyHostToDevice, st));
+  if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + a + b, C, M * N * 4, cudaMemcpyHostToDevice, st));
+  rc = gmm_impl(reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + a),
+                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(C, d + a + b, M * N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TIR_B200_OK;
+}
+
+int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                       float* Y, int accumulate) {
+  Geo g;
+  int rc = make_geo(desc, &g);
+  if (rc) return rc;
+  const int64_t xe = g.n * g.in[0] * g.in[1] * g.in[2] * g.ci;
+  const int64_t we = g.k[0] * g.k[1] * g.k[2] * (g.ci / g.g) * g.co;
+  const int64_t ye = g.n * g.out[0] * g.out[1] * g.out[2] * g.co;
+  const size_t xa = align256(xe * 2), wa = align256(we * 2), ya = align256(ye * 4);
+  char* d = nullptr;
+  rc = host_prepare(xa + wa + ya, &d);
+  if (rc) return rc;
+  cudaStream_t st = t_host.stream;
+  CUDA_TRY(cudaMemcpyAsync(d, X, xe * 2, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(d + xa, W, we * 2, cudaMemcpyHostToDevice, st));
+  if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + xa + wa, Y, ye * 4, cudaMemcpyHostToDevice, st));
+  rc = conv_impl(desc, reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + xa),
+                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TIR_B200_OK;
+}
+
+static int check_exact_flag() {
+  int flag = 0;
+  CUDA_TRY(cudaMemcpyAsync(&flag, t_host.dflag, sizeof(int), cudaMemcpyDeviceToHost, t_host.stream));
+  CUDA_TRY(cudaStreamSynchronize(t_host.stream));
+  if (flag) return set_err(TIR_B200_ERR_VALUE, "inexact f16 input: a value is not representable in fp16");
+  return TIR_B200_OK;
+}
+
+int tir_b200_gmm_host_f32(const float* A, const float* B, float* C, int64_t M, int64_t N, int64_t K,
+                          int accumulate) {
+  if (M < 0 || N < 0 || K < 0) return set_err(TIR_B200_ERR_VALUE, "gmm: negative extent");
+  const size_t a = align256(M * K * 2), b = align256(K * N * 2), c = align256(M * N * 4);
+  const size_t stage = align256(std::max(M * K, K * N) * 4);
+  char* d = nullptr;
+  int rc = host_prepare(a + b + c + stage, &d);
+  if (rc) return rc;
+  cudaStream_t st = t_host.stream;
+  CUDA_TRY(cudaMemsetAsync(t_host.dflag, 0, sizeof(int), st));
+  float* sg = reinterpret_cast<float*>(d + a + b + c);
+  rc = upload_f32_as_f16(A, M * K, sg, reinterpret_cast<uint16_t*>(d), st);
+  if (rc) return rc;
+  rc = upload_f32_as_f16(B, K * N, sg, reinterpret_cast<uint16_t*>(d + a), st);
+  if (rc) return rc;
+  rc = check_exact_flag();
+  if (rc) return rc;
+  if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + a + b, C, M * N * 4, cudaMemcpyHostToDevice, st));
+  rc = gmm_impl(reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + a),
+                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(C, d + a + b, M * N * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TIR_B200_OK;
+}
+
+int tir_b200_conv_host_f32(const tir_b200_conv_desc* desc, const float* X, const float* W, float* Y,
+                           int accumulate) {
+  Geo g;
+  int rc = make_geo(desc, &g);
+  if (rc) return rc;
+  const int64_t xe = g.n * g.in[0] * g.in[1] * g.in[2] * g.ci;
+  const int64_t we = g.k[0] * g.k[1] * g.k[2] * (g.ci / g.g) * g.co;
+  const int64_t ye = g.n * g.out[0] * g.out[1] * g.out[2] * g.co;
+  const size_t xa = align256(xe * 2), wa = align256(we * 2), ya = align256(ye * 4);
+  const size_t stage = align256(std::max(xe, we) * 4);
+  char* d = nullptr;
+  rc = host_prepare(xa + wa + ya + stage, &d);
+  if (rc) return rc;
+  cudaStream_t st = t_host.stream;
+  CUDA_TRY(cudaMemsetAsync(t_host.dflag, 0, sizeof(int), st));
+  float* sg = reinterpret_cast<float*>(d + xa + wa + ya);
+  rc = upload_f32_as_f16(X, xe, sg, reinterpret_cast<uint16_t*>(d), st);
+  if (rc) return rc;
+  rc = upload_f32_as_f16(W, we, sg, reinterpret_cast<uint16_t*>(d + xa), st);
+  if (rc) return rc;
+  rc = check_exact_flag();
+  if (rc) return rc;
+  if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + xa + wa, Y, ye * 4, cudaMemcpyHostToDevice, st));
+  rc = conv_impl(desc, reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + xa),
+                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, st);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return TIR_B200_OK;
+}
+
+void tir_b200_release_host_cache(void) {
+  if (t_host.dev >= 0) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(t_host.dev);
+    if (t_host.dbuf) cudaFree(t_host.dbuf);
+    if (t_host.dflag) cudaFree(t_host.dflag);
+    if (t_host.stream) cudaStreamDestroy(t_host.stream);
+    cudaSetDevice(cur);
+  }
+  t_host = HostCache{};
+}
+
+}  // extern "C"
