@@ -1,0 +1,489 @@
+"""Benchmark of the tensorized-operator hot path on B200 (contract: see DESIGN.md §Measurement).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--op C2D] [--no-ops] [--no-cpu]
+
+Headline workload (BASELINE.json configs[1]): C2D, ResNet-50 layer shape
+N=16, 56x56x64 -> 64, 3x3, stride 1, pad 1, fp16 in / fp32 accumulate / fp32 out,
+as one tcgen05 implicit-GEMM launch. A "step" = one operator pass over one
+batch. Inputs are resident in HBM; K steps rotate over enough input/output
+sets to exceed 2x the 126 MB L2, captured once in a CUDA graph (the launches
+are host-bound otherwise) and replayed between CUDA events on the launching
+stream. Under torchrun every rank runs its own replica ("replicas only":
+single ops do not shard) and the max time over ranks is
+reported.
+
+One JSON line on rank 0: the headline metric plus `ops` (the paper's full
+single-op sweep measured the same way), `roofline`, `cpu_baseline`, `e2e`
+(synchronous host-buffer C-ABI call: H2D + kernel + D2H), `clocks` and
+`gpu_launches`.
+
+--impl reference times the reference's own CPU implementation of the path —
+tir::run from /root/reference/proj (built into oracle/_ref by oracle/Makefile)
+on the host cores, rank 0 only, each step a bounded slice of the same C2D
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+HEADLINE = "C2D"
+L2_BYTES = 126 * 1024 * 1024
+METRIC = "per-op TFLOPS & % of B200 fp16 tensor peak (DEP: HBM GB/s) vs host-CPU ref"
+SPEC_TC_PEAK_TFLOPS = 2250.0
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+                "source": "fallback"}
+
+
+# ----------------------------------------------------------------------------- dist
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def init_dist(world, backend):
+    import torch.distributed as dist
+
+    if world > 1 and not dist.is_initialized():
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group(backend=backend)
+    return dist if world > 1 else None
+
+
+# ----------------------------------------------------------------------------- clocks
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms (B200_PROFILING.md)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms",
+                 "100", "-i", str(self.gpu)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                text=True)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        self.lines = []
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                out = ""
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": mx, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- workloads
+
+def op_spec(name):
+    import paper_2207_04296_b200 as tb
+
+    if name == "GMM":
+        return None
+    return tb.PAPER_SHAPES[name]
+
+
+def op_work(name):
+    """(flops, compulsory bytes, roofline bound) of one launch."""
+    import paper_2207_04296_b200 as tb
+
+    pk = peaks()
+    if name == "GMM":
+        M, N, K = tb.GMM_SHAPE
+        flops = 2 * M * N * K
+        byts = M * K * 2 + K * N * 2 + M * N * 4
+    else:
+        spec = op_spec(name)
+        flops = 2 * tb.useful_macs(spec)
+        byts = tb.compulsory_bytes(spec)
+    ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    bound = "hbm" if (name == "DEP" or flops / byts < ridge) else "tensor"
+    return flops, byts, bound
+
+
+class OpRunner:
+    """Device buffers (rotating sets > 2x L2) + one launch per step."""
+
+    def __init__(self, name, device):
+        import torch
+
+        import paper_2207_04296_b200 as tb
+
+        self.name = name
+        self.tb = tb
+        g = torch.Generator(device=device)
+        g.manual_seed(1234)
+        if name == "GMM":
+            M, N, K = tb.GMM_SHAPE
+            set_bytes = M * K * 2 + K * N * 2 + M * N * 4
+            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
+            self.A = [torch.randn(M, K, device=device, generator=g).half() for _ in range(self.sets)]
+            self.B = [torch.randn(K, N, device=device, generator=g).half() for _ in range(self.sets)]
+            self.C = [torch.empty(M, N, device=device) for _ in range(self.sets)]
+            self.fn = lambda i: tb.gmm(self.A[i], self.B[i], self.C[i])
+        else:
+            spec = op_spec(name)
+            self.spec = spec
+            xs, ws, ys = spec.x_shape(), spec.w_shape(), spec.y_shape()
+            n_x = math.prod(xs) * 2
+            n_y = math.prod(ys) * 4
+            self.sets = max(2, math.ceil(2 * L2_BYTES / (n_x + n_y)))
+            self.sets = min(self.sets, 64)
+            self.X = [torch.randn(*xs, device=device, generator=g).half() for _ in range(self.sets)]
+            self.W = torch.randn(*ws, device=device, generator=g).half()
+            self.Y = [torch.empty(*ys, device=device) for _ in range(self.sets)]
+            self.fn = lambda i: tb.conv(spec, self.X[i], self.W, self.Y[i])
+
+    def step(self, i):
+        self.fn(i % self.sets)
+
+
+def time_graph(runner, steps, warmup, dist, sampler_gpu):
+    """Returns (elapsed ms for `steps` launches = max over ranks, launches in graph, clocks)."""
+    import torch
+
+    tb = runner.tb
+    for i in range(warmup):
+        runner.step(i)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    tb.reset_launch_count()
+    with torch.cuda.graph(g, capture_error_mode="relaxed"):
+        for i in range(steps):
+            runner.step(i)
+    launches = tb.launch_count()
+    g.replay()  # graph warm-up (untimed)
+    torch.cuda.synchronize()
+    clocks = None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream = torch.cuda.current_stream()
+
+    def timed():
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0.record(stream)
+        g.replay()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        return e0.elapsed_time(e1)
+
+    if sampler_gpu is not None:
+        with ClockSampler(sampler_gpu) as cs:
+            t_end = time.time() + 0.5
+            while time.time() < t_end:  # sustained load around the timed region
+                g.replay()
+            ms = timed()
+            t_end = time.time() + 0.5
+            while time.time() < t_end:
+                g.replay()
+            torch.cuda.synchronize()
+        clocks = cs.summary()
+    else:
+        ms = timed()
+    if dist:
+        t = torch.tensor([ms], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    del g
+    return ms, launches, clocks
+
+
+def measure_e2e(name, steps):
+    """Synchronous host-buffer C-ABI call (tir_b200_conv_host / gmm_host): pinned fp16
+    inputs H2D, kernel, fp32 result D2H, every step. Host wall clock."""
+    import numpy as np
+    import torch
+
+    import paper_2207_04296_b200 as tb
+
+    rng = np.random.default_rng(7)
+    if name == "GMM":
+        M, N, K = tb.GMM_SHAPE
+        A = torch.from_numpy(rng.standard_normal((M, K), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
+        B = torch.from_numpy(rng.standard_normal((K, N), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
+        C = torch.empty((M, N), dtype=torch.float32).pin_memory().numpy()
+        fn = lambda: tb.gmm_host(A, B, C)  # noqa: E731
+        h2d, d2h = A.nbytes + B.nbytes, C.nbytes
+    else:
+        spec = op_spec(name)
+        X = torch.from_numpy(rng.standard_normal(spec.x_shape(), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
+        W = torch.from_numpy(rng.standard_normal(spec.w_shape(), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
+        Y = torch.empty(spec.y_shape(), dtype=torch.float32).pin_memory().numpy()
+        fn = lambda: tb.conv_host(spec, X, W, Y)  # noqa: E731
+        h2d, d2h = X.nbytes + W.nbytes, Y.nbytes
+    for _ in range(2):
+        fn()
+    n = max(3, min(steps, 50))
+    t0 = time.perf_counter()
+    for _ in range(n):
+        fn()
+    dt = (time.perf_counter() - t0) / n
+    flops, _, _ = op_work(name)
+    return {"value": round(flops / dt / 1e12, 4), "unit": "TFLOPS", "h2d_bytes_per_step": int(h2d),
+            "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 4), "steps": n,
+            "timing": "host wall clock around the synchronous C-ABI host-buffer call",
+            "api": "tir_b200_conv_host" if name != "GMM" else "tir_b200_gmm_host"}
+
+
+def traffic_from_profiles(name):
+    """dram read+write bytes per launch from the committed ncu --set full summary."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(name)
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU reference
+
+def cpu_reference_sample(name, budget_s, threads):
+    """tir::run (reference interpreter, oracle/_ref) on `threads` disjoint output
+    slices of the workload, concurrently. Returns (TFLOPS, seconds, sample text)."""
+    from oracle import ir_gen as G
+    from oracle import oracle as O
+
+    spec = op_spec(name)
+    ospec = G.ConvSpec(op=spec.op, n=spec.n, in_dhw=spec.in_dhw, ci=spec.ci, co=spec.co, k=spec.k,
+                       s=spec.s, p=spec.p, d=spec.d, groups=spec.groups,
+                       transposed=spec.transposed)
+    od, oh, ow = ospec.out_dhw()
+    macs_per_pixel = ospec.macs() // (ospec.n * od * oh * ow)
+    ns_per_mac = 1.3e-6  # survey-measured tir::run cost on conv
+    pix = max(1, int(budget_s / (macs_per_pixel * ns_per_mac)))
+    pix = min(pix, ow)
+    X = O.reference_tensor(ospec.x_shape(), 1)
+    W = O.reference_tensor(ospec.w_shape(), 2)
+    rows_total = ospec.n * od * oh
+    texts = []
+    for t in range(threads):
+        r = (t * 7919) % rows_total
+        texts.append(G.conv_source(ospec, rows=(r, r + 1), cols=(0, pix)))
+    wall = O.ref_run_many(texts, [X, W])
+    macs = threads * pix * macs_per_pixel
+    return 2 * macs / wall / 1e12, wall, (
+        f"{threads} concurrent tir::run slices of {name} image rows, {pix} output pixels x "
+        f"{macs_per_pixel} MACs each ({macs} MACs total)")
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import oracle as O
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtirref.so not built"}))
+        return
+    threads = os.cpu_count() or 1
+    total_budget = 150.0
+    per_step = max(0.5, total_budget / (args.steps + args.warmup))
+    for _ in range(args.warmup):
+        cpu_reference_sample(HEADLINE, per_step, threads)
+    vals, secs = [], 0.0
+    sample = ""
+    for _ in range(args.steps):
+        v, s, sample = cpu_reference_sample(HEADLINE, per_step, threads)
+        vals.append(v)
+        secs += s
+    value = statistics.mean(vals)
+    spec = op_spec(HEADLINE)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "TFLOPS", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": secs / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (reference distribution, workloads.h:170-184)",
+        "config": {"workload": f"{HEADLINE} N{spec.n} {spec.in_dhw[1]}x{spec.in_dhw[2]}x{spec.ci}->"
+                               f"{spec.co} 3x3 s1 p1 (bounded per-step sample)",
+                   "parallelism": "host threads"},
+        "cpu_baseline": {"value": value, "unit": "TFLOPS", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "TFLOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ----------------------------------------------------------------------------- main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default=HEADLINE)
+    ap.add_argument("--no-ops", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile", metavar="OP", help="eager launches of one op for ncu (no timing)")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    if args.profile:
+        import torch
+
+        r = OpRunner(args.profile, torch.device("cuda", 0))
+        for i in range(args.warmup + args.steps):
+            r.step(i)
+        torch.cuda.synchronize()
+        return
+
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = init_dist(world, "nccl")
+    device = torch.device("cuda", local)
+    pk = peaks()
+
+    name = args.op
+    runner = OpRunner(name, device)
+    ms, launches, clocks = time_graph(runner, args.steps, args.warmup, dist,
+                                      sampler_gpu=local if rank == 0 else None)
+    flops, byts, bound = op_work(name)
+    sec = ms / 1e3
+    value = flops * args.steps * world / sec / 1e12
+    kernel_s = sec / args.steps  # one launch per step
+    if bound == "hbm":
+        achieved, peak, unit = byts / kernel_s / 1e9, pk["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = flops / kernel_s / 1e12, pk["bf16_tflops"], "TFLOP/s"
+    n_sets = runner.sets
+    del runner
+    torch.cuda.empty_cache()
+
+    ops = {}
+    if not args.no_ops and rank == 0:
+        for other in ["GMM", "C1D", "C2D", "C3D", "DIL", "GRP", "T2D", "DEP"]:
+            try:
+                r = OpRunner(other, device)
+                k = max(10, min(args.steps, 100))
+                oms, ol, _ = time_graph(r, k, 3, None, None)
+                f, b, bd = op_work(other)
+                t = oms / 1e3 / k
+                ops[other] = {
+                    "tflops": round(f / t / 1e12, 2), "gbs": round(b / t / 1e9, 1),
+                    "us": round(t * 1e6, 3), "bound": bd,
+                    "frac_tensor_spec": round(f / t / 1e12 / SPEC_TC_PEAK_TFLOPS, 4),
+                    "frac_tensor_measured": round(f / t / 1e12 / pk["bf16_tflops"], 4),
+                    "frac_hbm": round(b / t / 1e9 / pk["hbm_gbs"], 4),
+                    "frac_roofline": round(min(1.0, (f / t) / min(pk["bf16_tflops"] * 1e12,
+                                                                   f / b * pk["hbm_gbs"] * 1e9)), 4),
+                    "launches_per_step": ol // k, "l2_sets": r.sets,
+                }
+                del r
+                torch.cuda.empty_cache()
+            except Exception as e:  # report, never hide
+                ops[other] = {"error": str(e)[:200]}
+
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        e2e = measure_e2e(name, args.steps)
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        try:
+            threads = os.cpu_count() or 1
+            v, s, sample = cpu_reference_sample(name, 10.0, threads)
+            cpu = {"value": v, "unit": "TFLOPS", "cores": threads, "kind": "reference",
+                   "sample": sample, "seconds": round(s, 2)}
+        except Exception as e:
+            cpu = {"value": None, "unit": "TFLOPS", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {e}"[:200]}
+
+    if rank == 0:
+        spec = op_spec(name)
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": "TFLOPS", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 6),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
+            "data": "synthetic N(0,1)->fp16 inputs created on device",
+            "config": {
+                "workload": (f"{name} N{spec.n} {spec.in_dhw[1]}x{spec.in_dhw[2]}x{spec.ci}->{spec.co} "
+                             f"{spec.k[1]}x{spec.k[2]} s{spec.s[2]} p{spec.p[2]}, fp16 in / fp32 acc / fp32 out"
+                             if spec else "GMM 1024^3"),
+                "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                "l2": f"rotating {n_sets} input/output sets > 2x L2 (126 MB)",
+                "timing": "CUDA graph of K launches, CUDA events on the launching stream",
+            },
+            "frac_of_spec_tensor_peak": round(value / world / SPEC_TC_PEAK_TFLOPS, 4),
+            "roofline": {"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": unit,
+                         "frac": round(achieved / peak, 4), "traffic": traffic_from_profiles(name),
+                         "algorithmic_bytes": byts, "algorithmic_flops": flops,
+                         "peak_source": pk["source"]},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "clocks": clocks,
+            "gpu_launches": launches,
+            "ops": ops,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -125,8 +125,9 @@ def gmm_source(m: int, n: int, k: int, rows=None, name: str = "gmm") -> str:
     )
 
 
-def conv_source(spec: ConvSpec, rows=None, name: str | None = None) -> str:
-    """Scalar program for C1D/C2D/C3D/DIL/GRP/T2D/DEP (see module doc)."""
+def conv_source(spec: ConvSpec, rows=None, name: str | None = None, cols=None) -> str:
+    """Scalar program for C1D/C2D/C3D/DIL/GRP/T2D/DEP (see module doc). `cols`
+    restricts the innermost output spatial loop (ow) to [c0, c1)."""
     r = spec.spatial_rank
     name = name or spec.op.lower()
     od, oh, ow = spec.out_dhw()
@@ -154,7 +155,8 @@ def conv_source(spec: ConvSpec, rows=None, name: str | None = None) -> str:
     ind = "    "
     lines.append(f"for row in 0..{r1 - r0} {{")
     depth = 1
-    lines.append(ind * depth + f"for {sp_names[-1]} in 0..{out_sp[-1]} {{")
+    c0, c1 = cols if cols else (0, out_sp[-1])
+    lines.append(ind * depth + f"for {sp_names[-1]} in 0..{c1 - c0} {{")
     depth += 1
     lines.append(ind * depth + f"for co in 0..{spec.co} {{")
     depth += 1
@@ -181,7 +183,7 @@ def conv_source(spec: ConvSpec, rows=None, name: str | None = None) -> str:
     binds.append(f"spatial vn: {spec.n} = {decomp['n']}")
     for nm, e in zip(sp_names[:-1], out_sp[:-1]):
         binds.append(f"spatial v{nm}: {e} = {decomp[nm]}")
-    binds.append(f"spatial v{sp_names[-1]}: {out_sp[-1]} = {sp_names[-1]}")
+    binds.append(f"spatial v{sp_names[-1]}: {out_sp[-1]} = {sp_names[-1]}" + (f" + {c0}" if c0 else ""))
     binds.append(f"spatial vco: {spec.co} = co")
     for nm, kk in zip(sp_names, ks):
         binds.append(f"reduce vr{nm}: {kk} = r{nm}")

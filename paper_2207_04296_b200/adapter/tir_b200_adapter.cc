@@ -1,0 +1,194 @@
+// tir_b200_adapter.cc — HostKernel adapter over the C-ABI (see the header).
+//
+// Packing: TensorView exposes only per-element accessors (interp.h:57-83), so
+// the views are packed row-major into host f32 staging (F16 values are f32
+// storage in the interpreter, ir.cc:36-47), handed to the synchronous
+// host-buffer entry points of include/tir_b200.h (which convert to fp16 on the
+// device and reject values fp16 cannot represent), and the accumulated output
+// is written back through set_f.
+#include "tir_b200_adapter.h"
+
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "tir/text.h"
+
+namespace tir_b200 {
+namespace {
+
+std::vector<int64_t> extents_of(const tir::TensorView& v) { return v.extents(); }
+
+int64_t cells_of(const std::vector<int64_t>& e) {
+  int64_t n = 1;
+  for (int64_t x : e) n *= x;
+  return n;
+}
+
+template <typename F>
+void for_each_index(const std::vector<int64_t>& ext, F&& f) {
+  if (cells_of(ext) == 0) return;
+  std::vector<int64_t> idx(ext.size(), 0);
+  for (int64_t flat = 0;; ++flat) {
+    f(idx, flat);
+    int d = static_cast<int>(idx.size()) - 1;
+    while (d >= 0 && ++idx[d] == ext[d]) idx[d--] = 0;
+    if (d < 0) break;
+  }
+}
+
+std::vector<float> pack(const tir::TensorView& v) {
+  std::vector<float> out(static_cast<size_t>(v.cells()));
+  for_each_index(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
+    out[static_cast<size_t>(flat)] = static_cast<float>(v.get_f(idx));
+  });
+  return out;
+}
+
+void unpack(tir::TensorView& v, const std::vector<float>& data) {
+  for_each_index(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
+    v.set_f(idx, data[static_cast<size_t>(flat)]);
+  });
+}
+
+[[noreturn]] void raise(int rc) {
+  const char* kind = rc == TIR_B200_ERR_VALUE         ? "ValueError"
+                     : rc == TIR_B200_ERR_UNSUPPORTED ? "UnsupportedShape"
+                                                      : "CudaError";
+  tir::throw_error(kind, tir_b200_last_error());
+}
+
+void require(bool ok, const std::string& msg) {
+  if (!ok) tir::throw_error("ValueError", msg);
+}
+
+void require_float(const tir::TensorView& v, const char* what) {
+  require(tir::dtype_is_float(v.dtype()), std::string(what) + " must be a float view");
+}
+
+std::vector<int64_t> conv_x_shape(const tir_b200_conv_desc& d, int rank) {
+  const int64_t sp[3] = {d.in_d, d.in_h, d.in_w};
+  std::vector<int64_t> s{d.n};
+  for (int i = 3 - rank; i < 3; ++i) s.push_back(sp[i]);
+  s.push_back(d.ci);
+  return s;
+}
+
+std::vector<int64_t> conv_w_shape(const tir_b200_conv_desc& d, int rank) {
+  const int64_t k[3] = {d.k_d, d.k_h, d.k_w};
+  std::vector<int64_t> s;
+  for (int i = 3 - rank; i < 3; ++i) s.push_back(k[i]);
+  if (d.op != TIR_B200_DEP) s.push_back(d.ci / d.groups);
+  s.push_back(d.co);
+  return s;
+}
+
+std::vector<int64_t> conv_y_shape(const tir_b200_conv_desc& d, int rank) {
+  int64_t out[3];
+  int rc = tir_b200_conv_out_shape(&d, out);
+  if (rc) raise(rc);
+  std::vector<int64_t> s{d.n};
+  for (int i = 3 - rank; i < 3; ++i) s.push_back(out[i]);
+  s.push_back(d.co);
+  return s;
+}
+
+int conv_rank(const tir_b200_conv_desc& d) {
+  return d.op == TIR_B200_C1D ? 1 : d.op == TIR_B200_C3D ? 3 : 2;
+}
+
+}  // namespace
+
+void register_gmm(tir::ExecContext& ctx, const std::string& name) {
+  ctx.register_host_kernel(name, [name](std::vector<tir::TensorView>& views) {
+    require(views.size() == 3, name + ": expects views [C, A, B]");
+    tir::TensorView& c = views[0];
+    const tir::TensorView& a = views[1];
+    const tir::TensorView& b = views[2];
+    require_float(c, "C");
+    require_float(a, "A");
+    require_float(b, "B");
+    const auto ce = c.extents(), ae = a.extents(), be = b.extents();
+    require(ce.size() == 2 && ae.size() == 2 && be.size() == 2, name + ": operands must be 2-D");
+    const int64_t M = ae[0], K = ae[1], N = be[1];
+    require(be[0] == K && ce[0] == M && ce[1] == N, name + ": operand extents do not form C[M,N] += A[M,K].B[K,N]");
+    std::vector<float> A = pack(a), B = pack(b), C = pack(c);
+    int rc = tir_b200_gmm_host_f32(A.data(), B.data(), C.data(), M, N, K, /*accumulate=*/1);
+    if (rc) raise(rc);
+    unpack(c, C);
+  });
+}
+
+void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b200_conv_desc& desc) {
+  // Validate once at registration; geometry errors surface here, not mid-run.
+  int64_t out[3];
+  int rc = tir_b200_conv_out_shape(&desc, out);
+  if (rc) raise(rc);
+  ctx.register_host_kernel(name, [name, desc](std::vector<tir::TensorView>& views) {
+    require(views.size() == 3, name + ": expects views [Y, X, W]");
+    tir::TensorView& y = views[0];
+    const tir::TensorView& x = views[1];
+    const tir::TensorView& w = views[2];
+    require_float(y, "Y");
+    require_float(x, "X");
+    require_float(w, "W");
+    const int r = conv_rank(desc);
+    require(x.extents() == conv_x_shape(desc, r), name + ": X view does not match the descriptor");
+    require(w.extents() == conv_w_shape(desc, r), name + ": W view does not match the descriptor");
+    require(y.extents() == conv_y_shape(desc, r), name + ": Y view does not match the descriptor");
+    std::vector<float> X = pack(x), W = pack(w), Y = pack(y);
+    int rc2 = tir_b200_conv_host_f32(&desc, X.data(), W.data(), Y.data(), /*accumulate=*/1);
+    if (rc2) raise(rc2);
+    unpack(y, Y);
+  });
+}
+
+std::string conv_intrin_name(const tir_b200_conv_desc& d) {
+  static const char* tags[] = {"gmm", "c1d", "c2d", "c3d", "dil", "grp", "t2d", "dep"};
+  const char* tag = (d.op >= 0 && d.op <= 7) ? tags[d.op] : "conv";
+  return std::string("b200.") + tag + ".s" + std::to_string(d.s_w) + "p" + std::to_string(d.p_w) +
+         "d" + std::to_string(d.d_w) + "g" + std::to_string(d.groups);
+}
+
+}  // namespace tir_b200
+
+// ---------------------------------------------------------------------------
+// C entry point for the drop-in tests (tests/test_dropin.py, ctypes): parse a
+// program in the reference grammar, register the B200 intrinsic(s) on a fresh
+// ExecContext and run the reference interpreter, which dispatches every
+// tensorized block to the GPU through the HostKernels above.
+extern "C" int tir_b200_adapter_run(const char* ir_text, const char* intrin,
+                                    const tir_b200_conv_desc* desc, int n_in,
+                                    const float* const* inputs, float* out, int64_t out_elems,
+                                    int64_t* intrinsic_calls, char* err, int errlen) {
+  try {
+    tir::PrimFuncPtr f = tir::parse_text(ir_text);
+    tir::ExecContext ctx;
+    if (desc) {
+      tir_b200::register_conv(ctx, intrin, *desc);
+    } else {
+      tir_b200::register_gmm(ctx, intrin);
+    }
+    auto in_params = tir::input_params(*f);
+    if (static_cast<int>(in_params.size()) != n_in)
+      tir::throw_error("ValueError", "input count mismatch");
+    std::vector<tir::TensorValue> vals;
+    for (int i = 0; i < n_in; ++i) {
+      tir::TensorValue t = tir::TensorValue::zeros(in_params[i]->dtype, in_params[i]->shape);
+      std::memcpy(t.data.data(), inputs[i], t.data.size());
+      vals.push_back(std::move(t));
+    }
+    auto outs = tir::run(*f, vals, ctx);
+    if (intrinsic_calls) *intrinsic_calls = ctx.counters.intrinsic_calls;
+    if (outs.empty() || outs[0].num_elements() != out_elems)
+      tir::throw_error("ValueError", "unexpected output shape");
+    std::memcpy(out, outs[0].data.data(), static_cast<size_t>(out_elems) * 4);
+    return 0;
+  } catch (const tir::Error& e) {
+    std::snprintf(err, static_cast<size_t>(errlen), "%s|%s", e.kind().c_str(), e.message().c_str());
+    return -1;
+  } catch (const std::exception& e) {
+    std::snprintf(err, static_cast<size_t>(errlen), "InternalError|%s", e.what());
+    return -1;
+  }
+}

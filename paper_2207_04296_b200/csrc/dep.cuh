@@ -33,17 +33,17 @@ struct DepParams {
 
 template <int VEC, int R>
 __global__ void __launch_bounds__(256) dep_kernel(const DepParams p) {
+  // 32-bit index math (the host guarantees n*ceil(oh/R)*ow*c/VEC < 2^31).
   const int cvecs = p.c / VEC;
-  const int64_t total = static_cast<int64_t>(p.n) * ((p.oh + R - 1) / R) * p.ow * cvecs;
-  for (int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; idx < total;
-       idx += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-    const int cv = static_cast<int>(idx % cvecs);
-    int64_t rest = idx / cvecs;
-    const int ox = static_cast<int>(rest % p.ow);
+  const int ohb = (p.oh + R - 1) / R;
+  const int total = p.n * ohb * p.ow * cvecs;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int cv = idx % cvecs;
+    int rest = idx / cvecs;
+    const int ox = rest % p.ow;
     rest /= p.ow;
-    const int ohb = (p.oh + R - 1) / R;
-    const int oyb = static_cast<int>(rest % ohb);
-    const int n = static_cast<int>(rest / ohb);
+    const int oyb = rest % ohb;
+    const int n = rest / ohb;
     const int oy0 = oyb * R;
     const int c0 = cv * VEC;
 

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -26,6 +27,7 @@ namespace {
 
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
+thread_local unsigned long long* g_trace = nullptr;
 
 int set_err(int code, const char* fmt, ...) {
   char buf[512];
@@ -208,12 +210,30 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   using Cfg = tb::IgemmCfg<BN>;
   const DeviceInfo di = device_info();
   const int budget = di.smem_optin - 1024 - 256;
-  p.stages = std::min(8, budget / Cfg::kStageBytes);
+  int nst_max = 0;
+  for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
+  const int keys = p.groups * p.tiles_n;  // distinct B panels
+  const int res_rows = nst_max * tb::kBK;
+  const int res_bytes = res_rows * BN * 2;
+  int grid = std::min(p.total_tiles, di.sms);
+  // Keep B resident when its whole K panel fits next to a >= 4-deep A ring and
+  // every CTA can be pinned to one (group, n-tile): grid a multiple of `keys`.
+  if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && keys <= di.sms &&
+      res_rows * Cfg::kBRowBytes < (1 << 18) && res_bytes + 4 * Cfg::kABytes <= budget) {
+    p.b_mode = tb::B_RESIDENT;
+    p.b_res_rows = res_rows;
+    p.stages = std::min(8, (budget - res_bytes) / Cfg::kABytes);
+    grid = std::min(p.total_tiles, di.sms / keys * keys);
+  } else {
+    p.b_res_rows = 0;
+    p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes));
+  }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
-  const size_t smem = Cfg::smem_bytes(p.stages);
+  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows);
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
-  const int grid = std::min(p.total_tiles, di.sms);
+  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
+  p.trace = g_trace;
   tb::igemm_tc_kernel<BN><<<grid, tb::kThreads, smem, stream>>>(p);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
@@ -299,7 +319,7 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   p.a_box_ch = 64;
   p.cig = static_cast<int32_t>(K);
   p.cb_per_tap = s.num_pieces;
-  p.b_contig = 1;
+  p.b_mode = tb::B_STREAM;
   p.k_rows = static_cast<int32_t>(K);
   p.w_kx = p.w_ky = 1;
   p.cog = static_cast<int32_t>(N);
@@ -461,7 +481,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
       s.a_dil[i] = static_cast<int32_t>(g.d[2 - i]);
     }
     s.num_pieces = static_cast<int32_t>(taps * p.cb_per_tap);
-    p.b_contig = 1;
+    p.b_mode = tb::B_STREAM;
     int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, box);
     if (rc) return rc;
     const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, di.sms);
@@ -482,7 +502,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   const int nclass = static_cast<int>(g.s[0] * g.s[1] * g.s[2]);
   if (nclass > tb::kMaxSub)
     return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: %d sub-pixel classes (max %d)", nclass, tb::kMaxSub);
-  p.b_contig = 0;
+  p.b_mode = tb::B_PIECES;
   int64_t m_max = 0;
   int ns = 0;
   for (int qd = 0; qd < g.s[0]; ++qd)
@@ -577,6 +597,7 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
                    (reinterpret_cast<uintptr_t>(Y) % 32 == 0);
   const int v = vec ? 8 : 1;
   const int64_t work = g.n * ((g.out[1] + R - 1) / R) * g.out[2] * (g.ci / v);
+  if (work >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many outputs");
   const int64_t blocks = std::min<int64_t>((work + 255) / 256, static_cast<int64_t>(di.sms) * 16);
   if (vec)
     tb::dep_kernel<8, R><<<static_cast<unsigned>(blocks), 256, 0, stream>>>(p);
@@ -589,7 +610,7 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
 
 int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
               const float* Yin, void* Y, int accumulate, int out_f16, cudaStream_t stream) {
-  Geo g;
+  Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
   if (!X || !W || !Y || (accumulate && !Yin)) return set_err(TIR_B200_ERR_VALUE, "conv: null operand");
@@ -650,12 +671,13 @@ int upload_f32_as_f16(const float* host, size_t n, float* dstage, uint16_t* d16,
 extern "C" {
 
 int tir_b200_version(void) { return 1; }
+void tir_b200_debug_set_trace(unsigned long long* dev_buf) { g_trace = dev_buf; }
 const char* tir_b200_last_error(void) { return g_err.c_str(); }
 int64_t tir_b200_launch_count(void) { return g_launches; }
 void tir_b200_reset_launch_count(void) { g_launches = 0; }
 
 int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]) {
-  Geo g;
+  Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
   for (int i = 0; i < 3; ++i) out_dhw[i] = g.out[i];
@@ -693,7 +715,7 @@ int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M,
 
 int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
                        float* Y, int accumulate) {
-  Geo g;
+  Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
   const int64_t xe = g.n * g.in[0] * g.in[1] * g.in[2] * g.ci;
@@ -751,7 +773,7 @@ int tir_b200_gmm_host_f32(const float* A, const float* B, float* C, int64_t M, i
 
 int tir_b200_conv_host_f32(const tir_b200_conv_desc* desc, const float* X, const float* W, float* Y,
                            int accumulate) {
-  Geo g;
+  Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
   const int64_t xe = g.n * g.in[0] * g.in[1] * g.in[2] * g.ci;
