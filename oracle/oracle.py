@@ -132,6 +132,23 @@ def tensors_close(a: np.ndarray, b: np.ndarray, rel_tol: float = 1e-5) -> bool:
     return bool(np.all(np.abs(a64 - b64) <= rel_tol * denom))
 
 
+def tensors_close_dot(a: np.ndarray, b: np.ndarray, abs_sum: np.ndarray, rel_tol: float = 1e-4,
+                      dot_tol: float = 1e-6) -> bool:
+    """D2 criterion for reductions evaluated in a different order: each element
+    must satisfy tensors_close (|x-y| <= rel_tol*max(|x|,|y|,1)) OR be within
+    dot_tol of its dot product's absolute sum sum|a_k*b_k| (`abs_sum`, the
+    oracle run on |A|, |B|). A reassociated fp32 sum of K terms is accurate
+    relative to sum|a*b|, not to the (possibly cancelled) result; 1e-6 is
+    ~16 ulp of fp32."""
+    if a.shape != b.shape:
+        return False
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    err = np.abs(a64 - b64)
+    denom = np.maximum(np.maximum(np.abs(a64), np.abs(b64)), 1.0)
+    ok = (err <= rel_tol * denom) | (err <= dot_tol * abs_sum.astype(np.float64))
+    return bool(np.all(ok))
+
+
 def tensors_bitwise_equal(a: np.ndarray, b: np.ndarray) -> bool:
     """Value equality as the reference defines it (get_f compared with !=, so
     +0 == -0)."""

@@ -76,7 +76,7 @@ def test_dropin_matches_scalar_program(cuda):
     b = O.normal_f16((K, N), 6)
     scalar, _ = O.ref_run(G.gmm_source(M, N, K), [a, b], (M, N))
     tensorized, _ = run(G.tensorized_gmm_source(M, N, K), "b200.gmm", [a, b], (M, N))
-    assert O.tensors_close(tensorized, scalar, 1e-4)
+    assert O.tensors_close_dot(tensorized, scalar, O.gmm(np.abs(a), np.abs(b)), 1e-4, 1e-6)
 
 
 @pytest.mark.parametrize("op", ["C2D", "GRP", "T2D", "DEP", "C1D", "DIL"])
