@@ -10,14 +10,20 @@
 // box_ch-channel slab on the fly) and B the HWIO weights viewed as [taps*CIg, CO]
 // (a zero-copy reshape).
 //
-// Roles (256 threads, 1 CTA per SM pass, grid = min(tiles, SMs*occupancy)):
-//   warp 0      TMA producer: A slab(s) + B tile per 64-deep K stage into a
-//               multi-stage smem ring (full/empty mbarriers, expect_tx bytes)
-//   warp 1      MMA issuer: 4 x tcgen05.mma.kind::f16 (M=128, N=BN, K=16) per
-//               stage into a TMEM fp32 accumulator; tcgen05.commit frees the slot
-//   warp 2      TMEM allocator (2 accumulators x BN columns, double-buffered)
-//   warps 4-7   epilogue: tcgen05.ld -> (+Yin) -> fp32/fp16 vector stores; the
+// Roles (288 threads = 9 warps, persistent, grid = min(tiles, SMs)):
+//   warps 0-3   epilogue: tcgen05.ld -> (+Yin) -> fp32/fp16 vector stores; the
 //               second accumulator lets tile i's epilogue overlap tile i+1's MMAs
+//               (warp w reads TMEM lanes 32*(w%4)..+31)
+//   warps 4-7   TMA producers: producer w fills stages st = w, w+4, ... of every
+//               tile (A slab(s) + B tile per 64-deep K stage) into one shared
+//               smem ring (full/empty mbarriers, expect_tx bytes). Measured on
+//               B200 (tools/l2bw.cu): an issuing thread completes about one TMA
+//               request per ~500 cycles regardless of its queue depth, while
+//               independent issuers scale linearly to the ~17 TB/s L2 roof — so
+//               the loads are spread over four issuers.
+//   warp 8      TMEM allocator + MMA issuer: 4 x tcgen05.mma.kind::f16
+//               (M=128, N=BN, K=16) per stage into a TMEM fp32 accumulator;
+//               tcgen05.commit frees the slot / publishes the accumulator
 //
 // K enumeration (must match the reference reduction domain, workloads.h:106-108):
 // k = tap * CIg + c with tap = (kd, kh, kw) row-major and c fastest, i.e. the
@@ -31,7 +37,9 @@ namespace tb {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;
-constexpr int kThreads = 256;
+constexpr int kThreads = 288;
+constexpr int kProducers = 4;
+constexpr int kMaxPieces = 2048;  // per-launch piece table entries (16 B each)
 constexpr int kMaxSub = 4;
 
 enum AMode : int32_t { A_TILED = 2, A_IM2COL3 = 3, A_IM2COL4 = 4, A_IM2COL5 = 5 };
@@ -56,6 +64,7 @@ struct SubProb {
   int32_t w_base[3], w_step[3];  // weight tap coordinate = base + t*step
   int32_t num_pieces;         // taps * cb_per_tap
   int32_t num_stages;         // ceil(num_pieces / pieces_per_stage)
+  int32_t piece_begin;        // offset of this sub-problem in the piece table
   int32_t o_st[3], o_b[3];    // output coordinate = idx*st + b (x, y, z)
 };
 
@@ -81,6 +90,7 @@ struct alignas(64) IgemmParams {
   int32_t out_f16;
   int32_t stages;      // smem ring depth
   int32_t b_res_rows;  // B_RESIDENT: rows of the resident panel (multiple of 64)
+  int32_t total_pieces;  // piece-table entries (sum of sub-problem num_pieces)
   void* Y;
   const float* Yin;
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
@@ -97,10 +107,16 @@ struct IgemmCfg {
   static constexpr uint32_t kBLayout = kBRowBytes == 128 ? 2u : kBRowBytes == 64 ? 4u : 6u;
   static constexpr uint32_t kIdesc = idesc_f16_f32(kBM, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
   // smem: [A ring: S x 16 KB][B ring: S x kBBytes | resident panel][barriers]
-  static size_t smem_bytes(int stages, int b_res_rows) {
+  // Epilogue transpose staging: per epilogue warp 32 rows x (32 + 4 pad) fp32
+  // plus the 32 output-row offsets.
+  static constexpr int kEpiStride = 36;
+  static constexpr int kEpiWarpBytes = 32 * kEpiStride * 4 + 32 * 8;
+  static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
+  static size_t smem_bytes(int stages, int b_res_rows, int pieces) {
     const size_t b = b_res_rows ? static_cast<size_t>(b_res_rows) * BN * 2
                                 : static_cast<size_t>(stages) * kBBytes;
-    return 1024 /*align slack*/ + static_cast<size_t>(stages) * kABytes + b + 256 /*barriers*/;
+    return 1024 /*align slack*/ + static_cast<size_t>(stages) * kABytes + b + kEpiBytes +
+           static_cast<size_t>(pieces) * sizeof(int4) + 256 /*barriers*/;
   }
 };
 
@@ -117,6 +133,27 @@ __device__ __forceinline__ void decompose_tile(const IgemmParams& p, int tile, i
   mt = rest / p.groups;
 }
 
+// Piece table entry: everything a producer needs for one TMA piece, computed
+// once per launch so the producer loop does no index arithmetic.
+//   x = channel offset within the group (cb * box)
+//   y = im2col offsets ox | oy << 16,   z = oz
+//   w = B row (B_PIECES: weight row of this tap/channel block)
+__device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& sp, int pc) {
+  const int cpt = p.cb_per_tap;
+  const int tap = pc / cpt, cb = pc - tap * cpt;
+  const int T0 = sp.taps[0], T1 = sp.taps[1];
+  const int tx = tap % T0, ty = (tap / T0) % T1, tz = tap / (T0 * T1);
+  const int wx = sp.w_base[0] + tx * sp.w_step[0];
+  const int wy = sp.w_base[1] + ty * sp.w_step[1];
+  const int wz = sp.w_base[2] + tz * sp.w_step[2];
+  int4 e;
+  e.x = cb * p.a_box_ch;
+  e.y = (tx * sp.a_dil[0]) | ((ty * sp.a_dil[1]) << 16);
+  e.z = tz * sp.a_dil[2];
+  e.w = ((wz * p.w_ky + wy) * p.w_kx + wx) * p.cig + cb * p.a_box_ch;
+  return e;
+}
+
 template <int BN>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tc_kernel(const __grid_constant__ IgemmParams p) {
@@ -130,7 +167,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB0 = smem + static_cast<size_t>(S) * Cfg::kABytes;
   const size_t b_bytes = b_res ? static_cast<size_t>(p.b_res_rows) * BN * 2
                                : static_cast<size_t>(S) * Cfg::kBBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(sB0 + b_bytes);
+  uint8_t* epi_smem = sB0 + b_bytes;
+  int4* pieces = reinterpret_cast<int4*>(epi_smem + Cfg::kEpiBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(pieces + p.total_pieces);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;   // [2]
   uint64_t* tempty = tfull + 2;  // [2]
@@ -139,6 +178,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
+  constexpr uint32_t kMmaWarp = 8;
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
@@ -152,13 +192,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     mbar_init(bres_full, 1);
     fence_barrier_init();
   }
-  if (warp == 0 && lane == 0) {
+  if (warp == 4 && lane == 0) {
     for (int i = 0; i < p.num_sub; ++i) prefetch_tmap(&p.tmA[i]);
     prefetch_tmap(&p.tmB);
   }
-  if (warp == 2) {
+  if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, Cfg::kTmemCols);
     tmem_relinquish();
+  }
+  // Piece table (all threads).
+  if (p.a_mode != A_TILED) {
+    for (int s = 0; s < p.num_sub; ++s) {
+      const SubProb& sp = p.sub[s];
+      for (int pc = threadIdx.x; pc < sp.num_pieces; pc += kThreads)
+        pieces[sp.piece_begin + pc] = make_piece(p, sp, pc);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -167,233 +215,218 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   unsigned long long* trace = (blockIdx.x == 0) ? p.trace : nullptr;
   if (trace && threadIdx.x == 0) trace[1023] = clock64();
+  uint64_t t_start = 0;
+  if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
-    // The whole warp runs the (warp-uniform) loop so addresses and coordinates
-    // stay in uniform registers; one elected lane issues mbarrier/TMA ops.
-    {
-      const int box = p.a_box_ch;
-      const int pps = kBK / box;
-      const uint32_t piece_bytes = kBM * box * 2;
-      const int cpt = p.cb_per_tap;
-      const int a_mode = p.a_mode;
-      const int b_mode = p.b_mode;
-      const uint32_t stage_tx = Cfg::kABytes + (b_mode == B_RESIDENT ? 0u : Cfg::kBBytes);
-      if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles && elect_one()) {
-        // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once.
-        int s0, mt0, g0, nt0;
-        decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
-        const int col0 = g0 * p.cog + nt0 * BN;
+  if (warp >= 4 && warp < 4 + kProducers) {
+    // ------------------------------------------------------------ producers
+    const int pw = static_cast<int>(warp) - 4;
+    const int box = p.a_box_ch;
+    const int pps = kBK / box;
+    const uint32_t piece_bytes = kBM * box * 2;
+    const int a_mode = p.a_mode;
+    const int b_mode = p.b_mode;
+    const uint32_t stage_tx = Cfg::kABytes + (b_mode == B_RESIDENT ? 0u : Cfg::kBBytes);
+    if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
+      // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once; the
+      // 64-row boxes are spread over the producers.
+      int s0, mt0, g0, nt0;
+      decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
+      const int col0 = g0 * p.cog + nt0 * BN;
+      if (pw == 0 && elect_one())
         mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
-        for (int r = 0; r < p.b_res_rows; r += kBK)
+      __syncwarp();
+      if (elect_one()) {
+        for (int r = pw * kBK; r < p.b_res_rows; r += kProducers * kBK)
 #pragma unroll
           for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
             tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
                             static_cast<size_t>(r) * Cfg::kBRowBytes,
                         &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
       }
-      uint32_t slot = 0, phase = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-        int s, mt, g, nt;
-        decompose_tile(p, tile, s, mt, g, nt);
-        const SubProb& sp = p.sub[s];
-        const CUtensorMap* tmA = &p.tmA[s];
-        const int m0 = mt * kBM;
-        int x = m0 % sp.gx, rest = m0 / sp.gx;
-        int y = rest % sp.gy;
-        rest /= sp.gy;
-        int z = rest % sp.gz;
-        const int n = rest / sp.gz;
-        const int cx = sp.a_lo[0] + x * sp.a_st[0];
-        const int cy = sp.a_lo[1] + y * sp.a_st[1];
-        const int cz = sp.a_lo[2] + z * sp.a_st[2];
-        const int col0 = g * p.cog + nt * BN;
-        const int T0 = sp.taps[0], T1 = sp.taps[1];
-        const int dx = sp.a_dil[0], dy = sp.a_dil[1], dz = sp.a_dil[2];
-        const int npieces = sp.num_pieces, nst = sp.num_stages;
-        const int cbase = g * p.cig;
-        // piece state: channel block, tap (tx, ty, tz), im2col offsets
-        int cb = 0, tx = 0, ty = 0, tz = 0, ox = 0, oy = 0, oz = 0, pc = 0;
-        for (int st = 0; st < nst; ++st, ++it) {
-          mbar_wait(&empty[slot], phase ^ 1);
-          if (trace && lane == 0 && it < 128) trace[2 * it] = clock64();
+      __syncwarp();
+    }
+    int it_base = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      int s, mt, g, nt;
+      decompose_tile(p, tile, s, mt, g, nt);
+      const SubProb& sp = p.sub[s];
+      const CUtensorMap* tmA = &p.tmA[s];
+      const int m0 = mt * kBM;
+      int x = m0 % sp.gx, rest = m0 / sp.gx;
+      int y = rest % sp.gy;
+      rest /= sp.gy;
+      int z = rest % sp.gz;
+      const int n = rest / sp.gz;
+      const int cx = sp.a_lo[0] + x * sp.a_st[0];
+      const int cy = sp.a_lo[1] + y * sp.a_st[1];
+      const int cz = sp.a_lo[2] + z * sp.a_st[2];
+      const int col0 = g * p.cog + nt * BN;
+      const int npieces = sp.num_pieces, nst = sp.num_stages;
+      const int cbase = g * p.cig;
+      const int4* ptab = pieces + sp.piece_begin;
+      for (int st = pw; st < nst; st += kProducers) {
+        const int it = it_base + st;
+        const uint32_t slot = static_cast<uint32_t>(it % S);
+        const uint32_t phase = static_cast<uint32_t>(it / S) & 1u;
+        mbar_wait(&empty[slot], phase ^ 1);
+        if (elect_one()) {
+          if (trace && it < 128) trace[2 * it] = clock64();
           uint8_t* sA = sA0 + slot * Cfg::kABytes;
           uint8_t* sB = sB0 + slot * Cfg::kBBytes;
-          const bool leader = elect_one();
-          if (leader) mbar_arrive_expect_tx(&full[slot], stage_tx);
-          if (trace && lane == 0 && it < 64) trace[768 + 4 * it] = clock64();
+          mbar_arrive_expect_tx(&full[slot], stage_tx);
           for (int j = 0; j < pps; ++j) {
-            const int c = cbase + cb * box;
+            const int pc = st * pps + j;
             void* dA = sA + j * piece_bytes;
-            if (!leader) {
-            } else if (a_mode == A_IM2COL4) {
-              tma_im2col_4d(dA, tmA, &full[slot], c, cx, cy, n, static_cast<uint16_t>(ox),
-                            static_cast<uint16_t>(oy));
-            } else if (a_mode == A_TILED) {
-              tma_load_2d(dA, tmA, &full[slot], c, m0);
+            if (a_mode == A_TILED) {
+              tma_load_2d(dA, tmA, &full[slot], pc * kBK, m0);
+              continue;
+            }
+            // Past the last piece: re-read the last real A piece (finite data)
+            // against zero B rows (B_STREAM/B_RESIDENT rows >= k_rows are OOB).
+            int4 e = ptab[pc < npieces ? pc : npieces - 1];
+            if (pc >= npieces) e.w = p.k_rows;
+            const int c = cbase + e.x;
+            const uint16_t ox = static_cast<uint16_t>(e.y & 0xFFFF);
+            const uint16_t oy = static_cast<uint16_t>(e.y >> 16);
+            if (a_mode == A_IM2COL4) {
+              tma_im2col_4d(dA, tmA, &full[slot], c, cx, cy, n, ox, oy);
             } else if (a_mode == A_IM2COL3) {
-              tma_im2col_3d(dA, tmA, &full[slot], c, cx, n, static_cast<uint16_t>(ox));
+              tma_im2col_3d(dA, tmA, &full[slot], c, cx, n, ox);
             } else {
-              tma_im2col_5d(dA, tmA, &full[slot], c, cx, cy, cz, n, static_cast<uint16_t>(ox),
-                            static_cast<uint16_t>(oy), static_cast<uint16_t>(oz));
+              tma_im2col_5d(dA, tmA, &full[slot], c, cx, cy, cz, n, ox, oy,
+                            static_cast<uint16_t>(e.z));
             }
-            if (trace && lane == 0 && it < 64 && j == 0) trace[768 + 4 * it + 1] = clock64();
             if (b_mode == B_PIECES) {
-              int row = p.k_rows;  // beyond the last piece: fully out of bounds -> zeros
-              if (pc < npieces) {
-                const int wx = sp.w_base[0] + tx * sp.w_step[0];
-                const int wy = sp.w_base[1] + ty * sp.w_step[1];
-                const int wz = sp.w_base[2] + tz * sp.w_step[2];
-                row = ((wz * p.w_ky + wy) * p.w_kx + wx) * p.cig + cb * box;
-              }
-              if (leader)
 #pragma unroll
-                for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-                  tma_load_2d(sB + ch * (kBK * Cfg::kBRowBytes) + j * box * Cfg::kBRowBytes,
-                              &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk, row);
-            }
-            // Advance to the next piece; past the end, keep re-reading the last
-            // real A piece (finite data) whose B rows are zero.
-            ++pc;
-            if (pc < npieces) {
-              if (++cb == cpt) {
-                cb = 0;
-                ox += dx;
-                if (++tx == T0) {
-                  tx = 0;
-                  ox = 0;
-                  oy += dy;
-                  if (++ty == T1) {
-                    ty = 0;
-                    oy = 0;
-                    oz += dz;
-                    ++tz;
-                  }
-                }
-              }
+              for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
+                tma_load_2d(sB + ch * (kBK * Cfg::kBRowBytes) + j * box * Cfg::kBRowBytes,
+                            &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk, e.w);
             }
           }
-          if (trace && lane == 0 && it < 64) trace[768 + 4 * it + 2] = clock64();
-          if (b_mode == B_STREAM && leader) {
+          if (b_mode == B_STREAM) {
 #pragma unroll
             for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
               tma_load_2d(sB + ch * (kBK * Cfg::kBRowBytes), &p.tmB, &full[slot],
                           col0 + ch * Cfg::kBChunk, st * kBK);
           }
-          if (trace && lane == 0 && it < 64) trace[768 + 4 * it + 3] = clock64();
-          __syncwarp();
-          if (trace && lane == 0 && it < 128) trace[2 * it + 1] = clock64();
-          if (++slot == static_cast<uint32_t>(S)) {
-            slot = 0;
-            phase ^= 1;
-          }
+          if (trace && it < 128) trace[2 * it + 1] = clock64();
         }
-      }
-    }
-  } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer
-    // Warp-uniform loop; one elected lane issues tcgen05.mma / commit.
-    {
-      // Descriptor templates; per stage/k only the 14-bit start-address field
-      // (bits 0-13, address >> 4) changes, so plain 64-bit adds update it.
-      uint32_t a_layout, a_sbo, a_lbo;
-      uint32_t a_koff[4];  // byte offset of k-step k within an A stage
-      switch (p.a_box_ch) {
-        case 64:
-          a_layout = 2; a_sbo = 1024; a_lbo = 16;
-          for (int k = 0; k < 4; ++k) a_koff[k] = 32 * k;
-          break;
-        case 32:
-          a_layout = 4; a_sbo = 512; a_lbo = 16;
-          for (int k = 0; k < 4; ++k) a_koff[k] = (k >> 1) * 8192 + (k & 1) * 32;
-          break;
-        case 16:
-          a_layout = 6; a_sbo = 256; a_lbo = 16;
-          for (int k = 0; k < 4; ++k) a_koff[k] = k * 4096;
-          break;
-        default:  // 8 channels: pieces 2k and 2k+1 form one K=16 step (no swizzle)
-          a_layout = 0; a_sbo = 128; a_lbo = 2048;
-          for (int k = 0; k < 4; ++k) a_koff[k] = k * 4096;
-          break;
-      }
-      const uint64_t adesc0 = smem_desc(smem_u32(sA0), a_lbo, a_sbo, a_layout);
-      const uint32_t b_lbo = b_res ? p.b_res_rows * Cfg::kBRowBytes : kBK * Cfg::kBRowBytes;
-      const uint64_t bdesc0 = smem_desc(smem_u32(sB0), b_lbo, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
-      constexpr uint32_t kBk = (16 * Cfg::kBRowBytes) >> 4;   // per k-step (16 rows)
-      constexpr uint32_t kBst = (kBK * Cfg::kBRowBytes) >> 4; // per 64-row stage (resident)
-      constexpr uint32_t kBslot = Cfg::kBBytes >> 4;          // per ring slot (streamed)
-      constexpr uint32_t kAslot = Cfg::kABytes >> 4;
-      if (b_res && static_cast<int>(blockIdx.x) < p.total_tiles) {
-        mbar_wait(bres_full, 0);
-        tc_fence_after();
-      }
-      uint32_t slot = 0, phase = 0, local = 0;
-      int it = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
-        int s, mt, g, nt;
-        decompose_tile(p, tile, s, mt, g, nt);
-        const int nst = p.sub[s].num_stages;
-        const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
-        mbar_wait(&tempty[acc], acc_phase ^ 1);
-        tc_fence_after();
-        const uint32_t tmem_d = tmem_base + acc * BN;
-        for (int st = 0; st < nst; ++st, ++it) {
-          mbar_wait(&full[slot], phase);
-          tc_fence_after();
-          if (trace && lane == 0 && it < 128) trace[256 + 2 * it] = clock64();
-          const uint64_t a = adesc0 + slot * kAslot;
-          const uint64_t b = bdesc0 + (b_res ? st * kBst : slot * kBslot);
-          if (elect_one()) {
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_f16(tmem_d, a + (a_koff[k] >> 4), b + k * kBk, Cfg::kIdesc, (st | k) != 0);
-            umma_commit(&empty[slot]);
-          }
-          __syncwarp();
-          if (trace && lane == 0 && it < 128) trace[256 + 2 * it + 1] = clock64();
-          if (++slot == static_cast<uint32_t>(S)) {
-            slot = 0;
-            phase ^= 1;
-          }
-        }
-        if (elect_one()) umma_commit(&tfull[acc]);
         __syncwarp();
       }
+      it_base += nst;
     }
-  } else if (warp >= 4) {
+  } else if (warp == kMmaWarp) {
+    // ------------------------------------------------------------ MMA issuer
+    // Descriptor templates; per stage/k only the 14-bit start-address field
+    // (bits 0-13, address >> 4) changes, so plain 64-bit adds update it.
+    uint32_t a_layout, a_sbo, a_lbo;
+    uint32_t a_koff[4];  // byte offset of k-step k within an A stage
+    switch (p.a_box_ch) {
+      case 64:
+        a_layout = 2; a_sbo = 1024; a_lbo = 16;
+        for (int k = 0; k < 4; ++k) a_koff[k] = 32 * k;
+        break;
+      case 32:
+        a_layout = 4; a_sbo = 512; a_lbo = 16;
+        for (int k = 0; k < 4; ++k) a_koff[k] = (k >> 1) * 8192 + (k & 1) * 32;
+        break;
+      case 16:
+        a_layout = 6; a_sbo = 256; a_lbo = 16;
+        for (int k = 0; k < 4; ++k) a_koff[k] = k * 4096;
+        break;
+      default:  // 8 channels: pieces 2k and 2k+1 form one K=16 step (no swizzle)
+        a_layout = 0; a_sbo = 128; a_lbo = 2048;
+        for (int k = 0; k < 4; ++k) a_koff[k] = k * 4096;
+        break;
+    }
+    const uint64_t adesc0 = smem_desc(smem_u32(sA0), a_lbo, a_sbo, a_layout);
+    const uint32_t b_lbo = b_res ? p.b_res_rows * Cfg::kBRowBytes : kBK * Cfg::kBRowBytes;
+    const uint64_t bdesc0 = smem_desc(smem_u32(sB0), b_lbo, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
+    constexpr uint32_t kBk = (16 * Cfg::kBRowBytes) >> 4;   // per k-step (16 rows)
+    constexpr uint32_t kBst = (kBK * Cfg::kBRowBytes) >> 4; // per 64-row stage (resident)
+    constexpr uint32_t kBslot = Cfg::kBBytes >> 4;          // per ring slot (streamed)
+    constexpr uint32_t kAslot = Cfg::kABytes >> 4;
+    if (b_res && static_cast<int>(blockIdx.x) < p.total_tiles) {
+      mbar_wait(bres_full, 0);
+      tc_fence_after();
+    }
+    uint32_t slot = 0, phase = 0, local = 0;
+    int it = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
+      int s, mt, g, nt;
+      decompose_tile(p, tile, s, mt, g, nt);
+      const int nst = p.sub[s].num_stages;
+      const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+      mbar_wait(&tempty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tmem_d = tmem_base + acc * BN;
+      for (int st = 0; st < nst; ++st, ++it) {
+        mbar_wait(&full[slot], phase);
+        tc_fence_after();
+        if (trace && lane == 0 && it < 128) trace[256 + 2 * it] = clock64();
+        const uint64_t a = adesc0 + slot * kAslot;
+        const uint64_t b = bdesc0 + (b_res ? st * kBst : slot * kBslot);
+        if (elect_one()) {
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_f16(tmem_d, a + (a_koff[k] >> 4), b + k * kBk, Cfg::kIdesc, (st | k) != 0);
+          umma_commit(&empty[slot]);
+        }
+        __syncwarp();
+        if (trace && lane == 0 && it < 128) trace[256 + 2 * it + 1] = clock64();
+        if (++slot == static_cast<uint32_t>(S)) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+      if (elect_one()) umma_commit(&tfull[acc]);
+      __syncwarp();
+    }
+  } else if (warp < 4) {
     // ------------------------------------------------------------ epilogue
+    // TMEM -> registers (thread = output row) -> smem transpose -> coalesced
+    // stores: each store instruction writes 4 full output-row segments of
+    // 32 columns (128 B fp32 / 64 B fp16) instead of 32 scattered 16 B pieces.
     const uint32_t q = warp & 3;
-    const uint32_t row = q * 32 + lane;
+    float* stg = reinterpret_cast<float*>(epi_smem + q * Cfg::kEpiWarpBytes);
+    int64_t* row_off = reinterpret_cast<int64_t*>(stg + 32 * Cfg::kEpiStride);
+    const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) &&
+                        ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
+                        (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
     uint32_t local = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
       int s, mt, g, nt;
       decompose_tile(p, tile, s, mt, g, nt);
       const SubProb& sp = p.sub[s];
       const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
+      // Output offset of this lane's row (-1 when past the sub-problem's end).
+      {
+        const int m = mt * kBM + static_cast<int>(q * 32 + lane);
+        int64_t off = -1;
+        if (m < sp.m_count) {
+          int x = m % sp.gx, rest = m / sp.gx;
+          int y = rest % sp.gy;
+          rest /= sp.gy;
+          int z = rest % sp.gz;
+          int n = rest / sp.gz;
+          const int ox = x * sp.o_st[0] + sp.o_b[0];
+          const int oy = y * sp.o_st[1] + sp.o_b[1];
+          const int oz = z * sp.o_st[2] + sp.o_b[2];
+          const int64_t pix = ((static_cast<int64_t>(n) * p.out_dims[2] + oz) * p.out_dims[1] + oy) *
+                                  p.out_dims[0] + ox;
+          off = pix * p.ldy + g * p.cog + nt * BN;
+        }
+        row_off[lane] = off;
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      if (trace && threadIdx.x == 128 && local < 64) trace[512 + 2 * local] = clock64();
+      if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
 
-      const int m = mt * kBM + static_cast<int>(row);
-      const bool row_ok = m < sp.m_count;
-      int64_t pix = 0;
-      if (row_ok) {
-        int x = m % sp.gx, rest = m / sp.gx;
-        int y = rest % sp.gy;
-        rest /= sp.gy;
-        int z = rest % sp.gz;
-        int n = rest / sp.gz;
-        const int ox = x * sp.o_st[0] + sp.o_b[0];
-        const int oy = y * sp.o_st[1] + sp.o_b[1];
-        const int oz = z * sp.o_st[2] + sp.o_b[2];
-        pix = ((static_cast<int64_t>(n) * p.out_dims[2] + oz) * p.out_dims[1] + oy) *
-                  p.out_dims[0] + ox;
-      }
       const int ncol0 = nt * BN;  // within group
-      const int64_t base = pix * p.ldy + g * p.cog + ncol0;
       constexpr int kChunk = BN < 32 ? BN : 32;
+      constexpr int kLanesPerRow = kChunk / 4;  // float4 per lane
+      constexpr int kRowsPerPass = 32 / kLanesPerRow;
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += kChunk) {
         uint32_t r[32];
@@ -402,73 +435,76 @@ __global__ void __launch_bounds__(kThreads, 1)
         else tmem_ld_32x32b_x16(taddr, r);
         tmem_ld_wait();
         const int valid = min(kChunk, p.cog - (ncol0 + c0));
-        if (!row_ok || valid <= 0) continue;
-        const int64_t off = base + c0;
-        float v[kChunk];
+        if (valid <= 0) continue;  // warp-uniform
+        __syncwarp();
+        float* my = stg + lane * Cfg::kEpiStride;
 #pragma unroll
-        for (int i = 0; i < kChunk; ++i) v[i] = __uint_as_float(r[i]);
-        const bool full_vec = valid == kChunk && (off & 7) == 0;
-        if (p.accumulate) {
-          const float* yin = p.Yin + off;
-          if (full_vec) {
-#pragma unroll
-            for (int i = 0; i < kChunk; i += 4) {
-              const float4 t = *reinterpret_cast<const float4*>(yin + i);
-              v[i] = t.x + v[i];
-              v[i + 1] = t.y + v[i + 1];
-              v[i + 2] = t.z + v[i + 2];
-              v[i + 3] = t.w + v[i + 3];
+        for (int i = 0; i < kChunk; i += 4)
+          *reinterpret_cast<float4*>(my + i) = make_float4(
+              __uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+              __uint_as_float(r[i + 3]));
+        __syncwarp();
+        const int col = (lane % kLanesPerRow) * 4;
+#pragma unroll 4
+        for (int rr = lane / kLanesPerRow; rr < 32; rr += kRowsPerPass) {
+          const int64_t ro = row_off[rr];
+          if (ro < 0 || col >= valid) continue;
+          const int64_t off = ro + c0 + col;
+          float4 v = *reinterpret_cast<const float4*>(stg + rr * Cfg::kEpiStride + col);
+          const bool vec = vec_ok && col + 4 <= valid;
+          if (p.accumulate) {
+            if (vec) {
+              const float4 t = *reinterpret_cast<const float4*>(p.Yin + off);
+              v.x = t.x + v.x; v.y = t.y + v.y; v.z = t.z + v.z; v.w = t.w + v.w;
+            } else {
+              float* vv = reinterpret_cast<float*>(&v);
+              for (int i = 0; i < 4 && col + i < valid; ++i) vv[i] = p.Yin[off + i] + vv[i];
             }
-          } else {
-#pragma unroll
-            for (int i = 0; i < kChunk; ++i)
-              if (i < valid) v[i] = yin[i] + v[i];
           }
-        }
-        if (p.out_f16) {
-          __half* y = reinterpret_cast<__half*>(p.Y) + off;
-          if (full_vec) {
-#pragma unroll
-            for (int i = 0; i < kChunk; i += 8) {
-              uint4 u;
-              __half2 h0 = __floats2half2_rn(v[i], v[i + 1]);
-              __half2 h1 = __floats2half2_rn(v[i + 2], v[i + 3]);
-              __half2 h2 = __floats2half2_rn(v[i + 4], v[i + 5]);
-              __half2 h3 = __floats2half2_rn(v[i + 6], v[i + 7]);
+          if (p.out_f16) {
+            __half* y = reinterpret_cast<__half*>(p.Y) + off;
+            if (vec) {
+              __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+              uint2 u;
               u.x = *reinterpret_cast<uint32_t*>(&h0);
               u.y = *reinterpret_cast<uint32_t*>(&h1);
-              u.z = *reinterpret_cast<uint32_t*>(&h2);
-              u.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(y + i) = u;
+              *reinterpret_cast<uint2*>(y) = u;
+            } else {
+              const float* vv = reinterpret_cast<const float*>(&v);
+              for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = __float2half_rn(vv[i]);
             }
           } else {
-#pragma unroll
-            for (int i = 0; i < kChunk; ++i)
-              if (i < valid) y[i] = __float2half_rn(v[i]);
-          }
-        } else {
-          float* y = reinterpret_cast<float*>(p.Y) + off;
-          if (full_vec) {
-#pragma unroll
-            for (int i = 0; i < kChunk; i += 4)
-              *reinterpret_cast<float4*>(y + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-          } else {
-#pragma unroll
-            for (int i = 0; i < kChunk; ++i)
-              if (i < valid) y[i] = v[i];
+            float* y = reinterpret_cast<float*>(p.Y) + off;
+            if (vec) {
+              *reinterpret_cast<float4*>(y) = v;
+            } else {
+              const float* vv = reinterpret_cast<const float*>(&v);
+              for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = vv[i];
+            }
           }
         }
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (trace && threadIdx.x == 128 && local < 64) trace[512 + 2 * local + 1] = clock64();
+      __syncwarp();
+      if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local + 1] = clock64();
     }
   }
 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 2) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if (warp == kMmaWarp) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    uint64_t t_end;
+    uint32_t smid;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    p.trace[2048 + 4 * blockIdx.x] = t_start;
+    p.trace[2048 + 4 * blockIdx.x + 1] = t_end;
+    p.trace[2048 + 4 * blockIdx.x + 2] = smid;
+    p.trace[2048 + 4 * blockIdx.x + 3] = (p.total_tiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+  }
 }
 
 }  // namespace tb

@@ -20,6 +20,7 @@
 
 #include "../../include/tir_b200.h"
 #include "dep.cuh"
+#include "halo.cuh"
 #include "igemm.cuh"
 #include "prep.cuh"
 
@@ -203,13 +204,37 @@ int workspace(size_t bytes, void** out) {
   return TIR_B200_OK;
 }
 
+// ------------------------------------------------------------------ launches
+
+// Programmatic dependent launch: the kernel may begin (prologue, TMEM alloc,
+// barrier init) while the previous kernel on the stream drains; it waits with
+// griddepcontrol.wait before touching global memory. Captured into CUDA graphs
+// as a programmatic edge. TIR_B200_NO_PDL=1 disables it.
+template <typename Params>
+cudaError_t launch_pdl(void (*kernel)(Params), int grid, int block, size_t smem, cudaStream_t stream,
+                       const Params& p) {
+  static const bool no_pdl = getenv("TIR_B200_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
 // ------------------------------------------------------------------ igemm launch
 
 template <int BN>
 int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   using Cfg = tb::IgemmCfg<BN>;
   const DeviceInfo di = device_info();
-  const int budget = di.smem_optin - 1024 - 256;
+  const int table = p.total_pieces * 16;
+  const int budget = di.smem_optin - 1024 - 256 - table - Cfg::kEpiBytes;
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
   const int keys = p.groups * p.tiles_n;  // distinct B panels
@@ -229,7 +254,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes));
   }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
-  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows);
+  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces);
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
@@ -269,9 +294,11 @@ void set_sub_identity(tb::SubProb& s) {
 
 int finalize_tiles(tb::IgemmParams& p, int bn) {
   p.tiles_n = static_cast<int32_t>((p.cog + bn - 1) / bn);
-  int64_t t = 0;
+  int64_t t = 0, pieces = 0;
   for (int i = 0; i < p.num_sub; ++i) {
     tb::SubProb& s = p.sub[i];
+    s.piece_begin = static_cast<int32_t>(pieces);
+    if (p.a_mode != tb::A_TILED) pieces += s.num_pieces;
     s.tiles_m = (s.m_count + tb::kBM - 1) / tb::kBM;
     s.tile_begin = static_cast<int32_t>(t);
     t += static_cast<int64_t>(s.tiles_m) * p.groups * p.tiles_n;
@@ -279,6 +306,10 @@ int finalize_tiles(tb::IgemmParams& p, int bn) {
     s.num_stages = (s.num_pieces + pps - 1) / pps;
   }
   if (t >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "too many tiles");
+  if (pieces > tb::kMaxPieces)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "reduction too deep: %lld TMA pieces (max %d)",
+                   static_cast<long long>(pieces), tb::kMaxPieces);
+  p.total_pieces = static_cast<int32_t>(pieces);
   p.total_tiles = static_cast<int32_t>(t);
   return TIR_B200_OK;
 }
@@ -388,6 +419,159 @@ int pick_box(int64_t cig) {
   for (int b : {64, 32, 16, 8})
     if (cig % b == 0) return b;
   return 0;
+}
+
+// ------------------------------------------------------------------ conv (halo, stride 1)
+
+constexpr int kNotEligible = -100;  // halo path declines; caller uses im2col
+
+template <int BN, int KH, int KW>
+int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
+  using Cfg = tb::HaloCfg<BN>;
+  const DeviceInfo di = device_info();
+  const int keys = p.groups * p.tiles_n;
+  if (keys > di.sms) return kNotEligible;
+  if (BN > 64 && p.b_rows * Cfg::kBRowBytes >= (1 << 18)) return kNotEligible;
+  const int fixed = 1024 + 256 + p.b_rows * BN * 2 + 2 * p.stage_bytes;
+  const int slab = p.slab_rows * 128;
+  const int stages = std::min(4, (di.smem_optin - fixed) / slab);
+  if (stages < 2) return kNotEligible;
+  p.stages = stages;
+  const size_t smem = Cfg::smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  int grid = std::min(p.total_tiles, di.sms / keys * keys);
+  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
+  p.trace = g_trace;
+  CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW>, grid, tb::kHaloThreads, smem, stream, p));
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+// Stride-1 2-D convolution as halo tiles (see halo.cuh). Returns kNotEligible
+// for shapes outside its envelope.
+int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
+                   int accumulate, int out_f16, cudaStream_t stream) {
+  if (getenv("TIR_B200_NO_HALO")) return kNotEligible;
+  if (g.transposed || g.in[0] != 1 || g.k[0] != 1 || g.p[0] != 0) return kNotEligible;
+  if (g.s[1] != 1 || g.s[2] != 1 || g.d[1] != g.d[2]) return kNotEligible;
+  const int64_t cig = g.ci / g.g, cog = g.co / g.g;
+  if (cig % 64 || g.co % 8) return kNotEligible;
+  if (accumulate && !Yin) return kNotEligible;
+  const int64_t d = g.d[1], KH = g.k[1], KW = g.k[2];
+  const int64_t OH = g.out[1], OW = g.out[2];
+  int64_t Wt, R;
+  if (OW + (KW - 1) * d <= 128) {
+    Wt = OW;
+    R = 128 / (OW + (KW - 1) * d);
+  } else {
+    Wt = 128 - (KW - 1) * d;
+    R = 1;
+    if (Wt < 16) return kNotEligible;
+  }
+  const int64_t Wv = Wt + (KW - 1) * d;
+  const int64_t HR = R + (KH - 1) * d;
+  if (Wv > 256 || HR > 256) return kNotEligible;
+  const int64_t max_off = (KH - 1) * d * Wv + (KW - 1) * d;
+  int64_t slab_rows = std::max(HR * Wv, max_off + 128);
+  slab_rows = (slab_rows + 7) / 8 * 8;
+  if (slab_rows > tb::kHaloMaxRows) return kNotEligible;
+  const int64_t taps = KH * KW;
+  const DeviceInfo di = device_info();
+
+  tb::HaloParams p;
+  std::memset(&p, 0, sizeof p);
+  p.n = static_cast<int32_t>(g.n);
+  p.oh = static_cast<int32_t>(OH);
+  p.ow = static_cast<int32_t>(OW);
+  p.co = static_cast<int32_t>(g.co);
+  p.cig = static_cast<int32_t>(cig);
+  p.cog = static_cast<int32_t>(cog);
+  p.groups = static_cast<int32_t>(g.g);
+  p.kh = static_cast<int32_t>(KH);
+  p.kw = static_cast<int32_t>(KW);
+  p.dil = static_cast<int32_t>(d);
+  p.pad_h = static_cast<int32_t>(g.p[1]);
+  p.pad_w = static_cast<int32_t>(g.p[2]);
+  p.R = static_cast<int32_t>(R);
+  p.Wt = static_cast<int32_t>(Wt);
+  p.Wv = static_cast<int32_t>(Wv);
+  p.HR = static_cast<int32_t>(HR);
+  p.tiles_w = static_cast<int32_t>((OW + Wt - 1) / Wt);
+  p.tiles_h = static_cast<int32_t>((OH + R - 1) / R);
+  p.cblocks = static_cast<int32_t>(cig / 64);
+  p.b_rows = static_cast<int32_t>(taps * cig);
+  p.slab_rows = static_cast<int32_t>(slab_rows);
+  p.accumulate = accumulate;
+  p.out_f16 = out_f16;
+  p.Y = Y;
+  p.Yin = Yin;
+  // N tile: whole group width up to 256 when that still fills the machine.
+  const int64_t spatial_tiles = g.n * p.tiles_h * p.tiles_w;
+  const int bn = choose_bn(cog, spatial_tiles, g.g, di.sms);
+  p.tiles_n = static_cast<int32_t>((cog + bn - 1) / bn);
+  const int64_t total = spatial_tiles * g.g * p.tiles_n;
+  if (total >= (1ll << 31)) return kNotEligible;
+  p.total_tiles = static_cast<int32_t>(total);
+  // X as 4-D [N, H, W, C] (C fastest), box {64, Wv, HR, 1}; OOB -> zero padding
+  {
+    const Driver* drv = driver();
+    if (!drv->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.ci), static_cast<cuuint64_t>(g.in[2]),
+                          static_cast<cuuint64_t>(g.in[1]), static_cast<cuuint64_t>(g.n)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.ci * 2),
+                             static_cast<cuuint64_t>(g.ci * 2 * g.in[2]),
+                             static_cast<cuuint64_t>(g.ci * 2 * g.in[2] * g.in[1])};
+    cuuint32_t box[4] = {64, static_cast<cuuint32_t>(Wv), static_cast<cuuint32_t>(HR), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = drv->tiled(&p.tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<uint16_t*>(X), dims,
+                            strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "halo X tensor map failed (%d)", (int)r);
+  }
+  p.b_box_rows = 64;
+  for (int rows : {256, 192, 128}) {
+    if (p.b_rows % rows == 0) {
+      p.b_box_rows = rows;
+      break;
+    }
+  }
+  int rc = encode_2d(&p.tmW, W, taps * cig, g.co, std::min(bn, 64), p.b_box_rows);
+  if (rc) return rc;
+  // Epilogue: TMA bulk stores of [R][Wt][32] boxes when a 32-column chunk never
+  // crosses a group (cog % 32 == 0 or a single group) and, for accumulate, Y is
+  // updated in place (reduce-add). Otherwise direct register stores.
+  p.store_mode = 0;
+  p.stage_bytes = 0;
+  if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || Yin == Y) &&
+      !getenv("TIR_B200_NO_TMA_STORE")) {
+    const Driver* drv = driver();
+    const int esz = out_f16 ? 2 : 4;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.co), static_cast<cuuint64_t>(OW),
+                          static_cast<cuuint64_t>(OH), static_cast<cuuint64_t>(g.n)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.co * esz),
+                             static_cast<cuuint64_t>(g.co * esz * OW),
+                             static_cast<cuuint64_t>(g.co * esz * OW * OH)};
+    cuuint32_t box[4] = {32, static_cast<cuuint32_t>(Wt), static_cast<cuuint32_t>(R), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = drv->tiled(&p.tmY, out_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                            4, Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            out_f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r == CUDA_SUCCESS) {
+      p.store_mode = accumulate ? 2 : 1;
+      p.stage_bytes = static_cast<int32_t>((R * Wt * 32 * esz + 1023) / 1024 * 1024);
+    }
+  }
+  const bool k3 = KH == 3 && KW == 3;
+  switch (bn) {
+    case 16: return k3 ? launch_halo_bn<16, 3, 3>(p, stream) : launch_halo_bn<16, 0, 0>(p, stream);
+    case 32: return k3 ? launch_halo_bn<32, 3, 3>(p, stream) : launch_halo_bn<32, 0, 0>(p, stream);
+    case 64: return k3 ? launch_halo_bn<64, 3, 3>(p, stream) : launch_halo_bn<64, 0, 0>(p, stream);
+    case 128: return k3 ? launch_halo_bn<128, 3, 3>(p, stream) : launch_halo_bn<128, 0, 0>(p, stream);
+    case 256: return k3 ? launch_halo_bn<256, 3, 3>(p, stream) : launch_halo_bn<256, 0, 0>(p, stream);
+  }
+  return kNotEligible;
 }
 
 int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,
@@ -619,6 +803,8 @@ int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t*
     if (!is_depthwise(g)) return set_err(TIR_B200_ERR_VALUE, "DEP requires groups == ci == co");
     return dep_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
   }
+  rc = conv_halo_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+  if (rc != kNotEligible) return rc;
   return conv_tc_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
 }
 

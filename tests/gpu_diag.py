@@ -43,6 +43,12 @@ CASES = {
     "dep_paper": ("conv", "DEP"),
     "dep_s2": ("conv", dict(op="DEP", n=2, in_dhw=(1, 28, 28), ci=96, co=96, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), groups=96)),
     "dil_paper": ("conv", "DIL"),
+    "halo_c2d_ci128": ("conv", dict(op="C2D", n=2, in_dhw=(1, 14, 14), ci=128, co=128, k=(1, 3, 3), p=(0, 1, 1))),
+    "halo_c2d_wide": ("conv", dict(op="C2D", n=1, in_dhw=(1, 6, 150), ci=64, co=64, k=(1, 3, 3), p=(0, 1, 1))),
+    "halo_c2d_dil2": ("conv", dict(op="C2D", n=2, in_dhw=(1, 20, 20), ci=64, co=32, k=(1, 3, 3), p=(0, 2, 2), d=(1, 2, 2))),
+    "halo_c2d_5x5_nopad": ("conv", dict(op="C2D", n=2, in_dhw=(1, 17, 19), ci=64, co=96, k=(1, 5, 5))),
+    "halo_grp_s1": ("conv", dict(op="GRP", n=2, in_dhw=(1, 12, 12), ci=128, co=128, k=(1, 3, 3), p=(0, 1, 1), groups=2)),
+    "halo_c2d_co256": ("conv", dict(op="C2D", n=1, in_dhw=(1, 28, 28), ci=64, co=256, k=(1, 3, 3), p=(0, 1, 1))),
 }
 
 

@@ -10,7 +10,7 @@ import paper_2207_04296_b200 as tb  # noqa: E402
 L = tb.lib()
 L.tir_b200_debug_set_trace.argtypes = [ctypes.c_void_p]
 dev = torch.device("cuda:0")
-buf = torch.zeros(1024, dtype=torch.int64, device=dev)
+buf = torch.zeros(8192, dtype=torch.int64, device=dev)
 
 
 def show(name, fn):
@@ -37,7 +37,20 @@ def show(name, fn):
         w = t[768 + 4 * it: 772 + 4 * it]
         if w[0] == 0:
             break
+        continue
         print("stage %2d  after_expect %7d  after_A %7d  before_B %7d  after_B %7d" % (it, *(x - t0 for x in w)))
+    ctas = [(t[2048 + 4 * i], t[2049 + 4 * i], t[2050 + 4 * i], t[2051 + 4 * i]) for i in range(1024)]
+    ctas = [c for c in ctas if c[0]]
+    if ctas:
+        t0g = min(c[0] for c in ctas)
+        ends = sorted((c[1] - t0g, c[3]) for c in ctas)
+        starts = sorted(c[0] - t0g for c in ctas)
+        print(f"grid {len(ctas)} CTAs: start spread {starts[0]}..{starts[-1]} ns; end min {ends[0][0]} median {ends[len(ends)//2][0]} max {ends[-1][0]} ns")
+        by_tiles = {}
+        for e, nt in ends:
+            by_tiles.setdefault(nt, []).append(e)
+        for nt, es in sorted(by_tiles.items()):
+            print(f"  CTAs with {nt} tiles: {len(es)}, end ns min {min(es)} max {max(es)}")
     for i in range(64):
         a, b = t[512 + 2 * i], t[513 + 2 * i]
         if a == 0:
