@@ -10,6 +10,10 @@
 // box_ch-channel slab on the fly) and B the HWIO weights viewed as [taps*CIg, CO]
 // (a zero-copy reshape).
 //
+// Stages hold KS sub-blocks of 64 K (KS = 1, 2 or 4, a template parameter):
+// one barrier round then covers 4*KS MMAs, amortising the ~400-cycle
+// wait/commit latency of the single MMA warp (tools/trace_igemm.py).
+//
 // Roles (288 threads = 9 warps, persistent, grid = min(tiles, SMs)):
 //   warps 0-3   epilogue: tcgen05.ld -> (+Yin) -> fp32/fp16 vector stores; the
 //               second accumulator lets tile i's epilogue overlap tile i+1's MMAs
@@ -36,7 +40,7 @@
 namespace tb {
 
 constexpr int kBM = 128;
-constexpr int kBK = 64;
+constexpr int kBK = 64;  // K per sub-block (one 128-byte swizzle row of fp16)
 constexpr int kThreads = 288;
 constexpr int kProducers = 4;
 constexpr int kMaxPieces = 2048;  // per-launch piece table entries (16 B each)
@@ -93,25 +97,28 @@ struct alignas(64) IgemmParams {
   int32_t total_pieces;  // piece-table entries (sum of sub-problem num_pieces)
   void* Y;
   const float* Yin;
+  int32_t store_mode;  // 0: generic row-offset stores, 1: TMA store, 2: TMA reduce-add (Y += tile)
+  CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
 };
 
-template <int BN>
+template <int BN, int KS>
 struct IgemmCfg {
-  static constexpr int kABytes = kBM * kBK * 2;          // 16 KB
-  static constexpr int kBBytes = kBK * BN * 2;           // 64 rows x BN
-  static constexpr int kTmemCols = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                   : (2 * BN <= 256) ? 256 : 512;
+  static constexpr int kSubA = kBM * kBK * 2;               // 16 KB per 64-deep sub-block
+  static constexpr int kABytes = KS * kSubA;
+  static constexpr int kBRows = KS * kBK;                   // B rows per stage
+  static constexpr int kBBytes = kBRows * BN * 2;
+  static constexpr int kNacc = (4 * BN <= 512) ? 4 : 2;     // TMEM accumulator buffers
+  static constexpr int kTmemCols = (kNacc * BN <= 32) ? 32 : (kNacc * BN <= 64) ? 64
+                                   : (kNacc * BN <= 128) ? 128 : (kNacc * BN <= 256) ? 256 : 512;
   static constexpr int kBChunk = BN < 64 ? BN : 64;        // columns per B TMA box
   static constexpr int kBRowBytes = kBChunk * 2;           // 128 / 64 / 32
   static constexpr uint32_t kBLayout = kBRowBytes == 128 ? 2u : kBRowBytes == 64 ? 4u : 6u;
   static constexpr uint32_t kIdesc = idesc_f16_f32(kBM, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
-  // smem: [A ring: S x 16 KB][B ring: S x kBBytes | resident panel][barriers]
-  // Epilogue transpose staging: per epilogue warp 32 rows x (32 + 4 pad) fp32
-  // plus the 32 output-row offsets.
-  static constexpr int kEpiStride = 36;
-  static constexpr int kEpiWarpBytes = 32 * kEpiStride * 4 + 32 * 8;
+  // epilogue staging: per epilogue warp two 4 KB buffers (32 rows x 32 fp32)
+  static constexpr int kEpiWarpBytes = 8192;
   static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
+  // smem: [A ring][B ring | resident panel][epilogue staging][piece table][barriers]
   static size_t smem_bytes(int stages, int b_res_rows, int pieces) {
     const size_t b = b_res_rows ? static_cast<size_t>(b_res_rows) * BN * 2
                                 : static_cast<size_t>(stages) * kBBytes;
@@ -154,10 +161,10 @@ __device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& 
   return e;
 }
 
-template <int BN>
+template <int BN, int KS>
 __global__ void __launch_bounds__(kThreads, 1)
     igemm_tc_kernel(const __grid_constant__ IgemmParams p) {
-  using Cfg = IgemmCfg<BN>;
+  using Cfg = IgemmCfg<BN, KS>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -167,13 +174,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sB0 = smem + static_cast<size_t>(S) * Cfg::kABytes;
   const size_t b_bytes = b_res ? static_cast<size_t>(p.b_res_rows) * BN * 2
                                : static_cast<size_t>(S) * Cfg::kBBytes;
-  uint8_t* epi_smem = sB0 + b_bytes;
+  uint8_t* epi_smem = sB0 + b_bytes;  // 1024-aligned (all preceding sizes are)
   int4* pieces = reinterpret_cast<int4*>(epi_smem + Cfg::kEpiBytes);
   uint64_t* full = reinterpret_cast<uint64_t*>(pieces + p.total_pieces);
   uint64_t* empty = full + S;
-  uint64_t* tfull = empty + S;   // [2]
-  uint64_t* tempty = tfull + 2;  // [2]
-  uint64_t* bres_full = tempty + 2;
+  uint64_t* tfull = empty + S;            // [kNacc]
+  uint64_t* tempty = tfull + Cfg::kNacc;  // [kNacc]
+  uint64_t* bres_full = tempty + Cfg::kNacc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bres_full + 1);
 
   const uint32_t warp = warp_id();
@@ -185,16 +192,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128);
     }
     mbar_init(bres_full, 1);
     fence_barrier_init();
-  }
-  if (warp == 4 && lane == 0) {
-    for (int i = 0; i < p.num_sub; ++i) prefetch_tmap(&p.tmA[i]);
-    prefetch_tmap(&p.tmB);
   }
   if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, Cfg::kTmemCols);
@@ -212,6 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
 
   unsigned long long* trace = (blockIdx.x == 0) ? p.trace : nullptr;
   if (trace && threadIdx.x == 0) trace[1023] = clock64();
@@ -220,16 +224,20 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp >= 4 && warp < 4 + kProducers) {
     // ------------------------------------------------------------ producers
+    pdl_wait();  // operands may be produced by the preceding kernel
     const int pw = static_cast<int>(warp) - 4;
+    // At most S producers: a producer's consecutive stages it and it + nprod hit
+    // slots at most one phase apart only if nprod <= S (mbarrier parity is 1 bit).
+    const int nprod = S < kProducers ? S : kProducers;
     const int box = p.a_box_ch;
-    const int pps = kBK / box;
+    const int pps = KS * (kBK / box);  // pieces per stage
     const uint32_t piece_bytes = kBM * box * 2;
     const int a_mode = p.a_mode;
     const int b_mode = p.b_mode;
     const uint32_t stage_tx = Cfg::kABytes + (b_mode == B_RESIDENT ? 0u : Cfg::kBBytes);
     if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
       // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once; the
-      // 64-row boxes are spread over the producers.
+      // stage-row boxes are spread over the producers.
       int s0, mt0, g0, nt0;
       decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
       const int col0 = g0 * p.cog + nt0 * BN;
@@ -237,7 +245,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
       __syncwarp();
       if (elect_one()) {
-        for (int r = pw * kBK; r < p.b_res_rows; r += kProducers * kBK)
+        for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)  // one-shot
 #pragma unroll
           for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
             tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
@@ -265,7 +273,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int npieces = sp.num_pieces, nst = sp.num_stages;
       const int cbase = g * p.cig;
       const int4* ptab = pieces + sp.piece_begin;
-      for (int st = pw; st < nst; st += kProducers) {
+      // producer pw owns global stages it = pw (mod nprod), so its consecutive
+      // stages are exactly nprod apart even across tile boundaries
+      const int st0 = ((pw - it_base) % nprod + nprod) % nprod;
+      for (int st = st0; pw < nprod && st < nst; st += nprod) {
         const int it = it_base + st;
         const uint32_t slot = static_cast<uint32_t>(it % S);
         const uint32_t phase = static_cast<uint32_t>(it / S) & 1u;
@@ -283,7 +294,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               continue;
             }
             // Past the last piece: re-read the last real A piece (finite data)
-            // against zero B rows (B_STREAM/B_RESIDENT rows >= k_rows are OOB).
+            // against zero B rows (rows >= k_rows are out of bounds -> 0).
             int4 e = ptab[pc < npieces ? pc : npieces - 1];
             if (pc >= npieces) e.w = p.k_rows;
             const int c = cbase + e.x;
@@ -300,15 +311,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (b_mode == B_PIECES) {
 #pragma unroll
               for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-                tma_load_2d(sB + ch * (kBK * Cfg::kBRowBytes) + j * box * Cfg::kBRowBytes,
+                tma_load_2d(sB + ch * (Cfg::kBRows * Cfg::kBRowBytes) + j * box * Cfg::kBRowBytes,
                             &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk, e.w);
             }
           }
           if (b_mode == B_STREAM) {
 #pragma unroll
             for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-              tma_load_2d(sB + ch * (kBK * Cfg::kBRowBytes), &p.tmB, &full[slot],
-                          col0 + ch * Cfg::kBChunk, st * kBK);
+              tma_load_2d(sB + ch * (Cfg::kBRows * Cfg::kBRowBytes), &p.tmB, &full[slot],
+                          col0 + ch * Cfg::kBChunk, st * Cfg::kBRows);
           }
           if (trace && it < 128) trace[2 * it + 1] = clock64();
         }
@@ -321,7 +332,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // Descriptor templates; per stage/k only the 14-bit start-address field
     // (bits 0-13, address >> 4) changes, so plain 64-bit adds update it.
     uint32_t a_layout, a_sbo, a_lbo;
-    uint32_t a_koff[4];  // byte offset of k-step k within an A stage
+    uint32_t a_koff[4];  // byte offset of k-step k within a 64-deep A sub-block
     switch (p.a_box_ch) {
       case 64:
         a_layout = 2; a_sbo = 1024; a_lbo = 16;
@@ -341,23 +352,24 @@ __global__ void __launch_bounds__(kThreads, 1)
         break;
     }
     const uint64_t adesc0 = smem_desc(smem_u32(sA0), a_lbo, a_sbo, a_layout);
-    const uint32_t b_lbo = b_res ? p.b_res_rows * Cfg::kBRowBytes : kBK * Cfg::kBRowBytes;
+    const uint32_t b_lbo = b_res ? p.b_res_rows * Cfg::kBRowBytes : Cfg::kBRows * Cfg::kBRowBytes;
     const uint64_t bdesc0 = smem_desc(smem_u32(sB0), b_lbo, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
-    constexpr uint32_t kBk = (16 * Cfg::kBRowBytes) >> 4;   // per k-step (16 rows)
-    constexpr uint32_t kBst = (kBK * Cfg::kBRowBytes) >> 4; // per 64-row stage (resident)
-    constexpr uint32_t kBslot = Cfg::kBBytes >> 4;          // per ring slot (streamed)
+    constexpr uint32_t kBk = (16 * Cfg::kBRowBytes) >> 4;            // per k-step (16 rows)
+    constexpr uint32_t kBsub = (kBK * Cfg::kBRowBytes) >> 4;         // per 64-row sub-block
+    constexpr uint32_t kBst = (Cfg::kBRows * Cfg::kBRowBytes) >> 4;  // per stage (resident)
+    constexpr uint32_t kBslot = Cfg::kBBytes >> 4;                   // per ring slot
     constexpr uint32_t kAslot = Cfg::kABytes >> 4;
+    constexpr uint32_t kAsub = Cfg::kSubA >> 4;
     if (b_res && static_cast<int>(blockIdx.x) < p.total_tiles) {
       mbar_wait(bres_full, 0);
       tc_fence_after();
     }
-    uint32_t slot = 0, phase = 0, local = 0;
+    uint32_t slot = 0, phase = 0, acc = 0, acc_phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
       int s, mt, g, nt;
       decompose_tile(p, tile, s, mt, g, nt);
       const int nst = p.sub[s].num_stages;
-      const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
@@ -369,8 +381,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint64_t b = bdesc0 + (b_res ? st * kBst : slot * kBslot);
         if (elect_one()) {
 #pragma unroll
-          for (int k = 0; k < kBK / 16; ++k)
-            umma_f16(tmem_d, a + (a_koff[k] >> 4), b + k * kBk, Cfg::kIdesc, (st | k) != 0);
+          for (int u = 0; u < KS; ++u)
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
+                       Cfg::kIdesc, (st | u | k) != 0);
           umma_commit(&empty[slot]);
         }
         __syncwarp();
@@ -382,112 +397,179 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       if (elect_one()) umma_commit(&tfull[acc]);
       __syncwarp();
+      if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   } else if (warp < 4) {
     // ------------------------------------------------------------ epilogue
-    // TMEM -> registers (thread = output row) -> smem transpose -> coalesced
-    // stores: each store instruction writes 4 full output-row segments of
-    // 32 columns (128 B fp32 / 64 B fp16) instead of 32 scattered 16 B pieces.
+    pdl_wait();  // Y / Yin may be in use by the preceding kernel
     const uint32_t q = warp & 3;
-    float* stg = reinterpret_cast<float*>(epi_smem + q * Cfg::kEpiWarpBytes);
-    int64_t* row_off = reinterpret_cast<int64_t*>(stg + 32 * Cfg::kEpiStride);
-    const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) &&
-                        ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
-                        (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
-    uint32_t local = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
-      int s, mt, g, nt;
-      decompose_tile(p, tile, s, mt, g, nt);
-      const SubProb& sp = p.sub[s];
-      const uint32_t acc = local & 1, acc_phase = (local >> 1) & 1;
-      // Output offset of this lane's row (-1 when past the sub-problem's end).
-      {
-        const int m = mt * kBM + static_cast<int>(q * 32 + lane);
-        int64_t off = -1;
-        if (m < sp.m_count) {
-          int x = m % sp.gx, rest = m / sp.gx;
-          int y = rest % sp.gy;
-          rest /= sp.gy;
-          int z = rest % sp.gz;
-          int n = rest / sp.gz;
-          const int ox = x * sp.o_st[0] + sp.o_b[0];
-          const int oy = y * sp.o_st[1] + sp.o_b[1];
-          const int oz = z * sp.o_st[2] + sp.o_b[2];
-          const int64_t pix = ((static_cast<int64_t>(n) * p.out_dims[2] + oz) * p.out_dims[1] + oy) *
-                                  p.out_dims[0] + ox;
-          off = pix * p.ldy + g * p.cog + nt * BN;
-        }
-        row_off[lane] = off;
-      }
-      mbar_wait(&tfull[acc], acc_phase);
-      tc_fence_after();
-      if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
-
-      const int ncol0 = nt * BN;  // within group
-      constexpr int kChunk = BN < 32 ? BN : 32;
-      constexpr int kLanesPerRow = kChunk / 4;  // float4 per lane
-      constexpr int kRowsPerPass = 32 / kLanesPerRow;
+    uint8_t* wbuf = epi_smem + q * Cfg::kEpiWarpBytes;
+    uint32_t acc = 0, acc_phase = 0, chunk = 0;
+    if (p.store_mode) {
+      // TMA store: thread = tile row (tcgen05.ld 32x32b); each warp stages its
+      // 32 rows x 32 columns (SW128 / SW64 swizzled, conflict-free) and issues
+      // one bulk tensor store (or reduce-add for accumulate) per chunk; two
+      // staging buffers per warp. Row-linear outputs only (GMM, forward conv).
+      const int line_bytes = p.out_f16 ? 64 : 128;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        int s, mt, g, nt;
+        decompose_tile(p, tile, s, mt, g, nt);
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        constexpr int kCols = BN < 32 ? BN : 32;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += kChunk) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN + c0;
-        if (kChunk == 32) tmem_ld_32x32b_x32(taddr, r);
-        else tmem_ld_32x32b_x16(taddr, r);
-        tmem_ld_wait();
-        const int valid = min(kChunk, p.cog - (ncol0 + c0));
-        if (valid <= 0) continue;  // warp-uniform
-        __syncwarp();
-        float* my = stg + lane * Cfg::kEpiStride;
-#pragma unroll
-        for (int i = 0; i < kChunk; i += 4)
-          *reinterpret_cast<float4*>(my + i) = make_float4(
-              __uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
-              __uint_as_float(r[i + 3]));
-        __syncwarp();
-        const int col = (lane % kLanesPerRow) * 4;
-#pragma unroll 4
-        for (int rr = lane / kLanesPerRow; rr < 32; rr += kRowsPerPass) {
-          const int64_t ro = row_off[rr];
-          if (ro < 0 || col >= valid) continue;
-          const int64_t off = ro + c0 + col;
-          float4 v = *reinterpret_cast<const float4*>(stg + rr * Cfg::kEpiStride + col);
-          const bool vec = vec_ok && col + 4 <= valid;
-          if (p.accumulate) {
-            if (vec) {
-              const float4 t = *reinterpret_cast<const float4*>(p.Yin + off);
-              v.x = t.x + v.x; v.y = t.y + v.y; v.z = t.z + v.z; v.w = t.w + v.w;
-            } else {
-              float* vv = reinterpret_cast<float*>(&v);
-              for (int i = 0; i < 4 && col + i < valid; ++i) vv[i] = p.Yin[off + i] + vv[i];
-            }
-          }
+        for (int c0 = 0; c0 < BN; c0 += kCols, ++chunk) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
+          tmem_ld_wait();
+          if (nt * BN + c0 >= p.cog) continue;  // warp-uniform: chunk past the group
+          uint8_t* buf = wbuf + (chunk & 1) * 4096;
+          __syncwarp();  // lane 0 has retired the store that last read `buf`
+          uint8_t* dst = buf + lane * line_bytes;
           if (p.out_f16) {
-            __half* y = reinterpret_cast<__half*>(p.Y) + off;
-            if (vec) {
-              __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
-              uint2 u;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint4 u;
+              __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * c]), __uint_as_float(r[8 * c + 1]));
+              __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * c + 2]), __uint_as_float(r[8 * c + 3]));
+              __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * c + 4]), __uint_as_float(r[8 * c + 5]));
+              __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * c + 6]), __uint_as_float(r[8 * c + 7]));
               u.x = *reinterpret_cast<uint32_t*>(&h0);
               u.y = *reinterpret_cast<uint32_t*>(&h1);
-              *reinterpret_cast<uint2*>(y) = u;
-            } else {
-              const float* vv = reinterpret_cast<const float*>(&v);
-              for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = __float2half_rn(vv[i]);
+              u.z = *reinterpret_cast<uint32_t*>(&h2);
+              u.w = *reinterpret_cast<uint32_t*>(&h3);
+              *reinterpret_cast<uint4*>(dst + ((c ^ ((lane >> 1) & 3)) << 4)) = u;  // SW64
             }
           } else {
-            float* y = reinterpret_cast<float*>(p.Y) + off;
-            if (vec) {
-              *reinterpret_cast<float4*>(y) = v;
-            } else {
-              const float* vv = reinterpret_cast<const float*>(&v);
-              for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = vv[i];
-            }
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<uint4*>(dst + ((c ^ (lane & 7)) << 4)) =
+                  make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);  // SW128
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int col = g * p.cog + nt * BN + c0;
+            const int row = mt * kBM + static_cast<int>(q) * 32;
+            if (p.store_mode == 2) tma_reduce_add_2d(&p.tmY, buf, col, row);
+            else tma_store_2d(&p.tmY, buf, col, row);
+            tma_store_commit();
+            tma_store_wait_read<1>();
           }
         }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
       }
-      tc_fence_before();
-      mbar_arrive(&tempty[acc]);
-      __syncwarp();
-      if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local + 1] = clock64();
+      if (lane == 0) tma_store_wait_all<0>();
+    } else {
+      // Generic: TMEM -> registers (thread = output row) -> smem transpose ->
+      // coalesced stores of 32-column row segments at per-row output offsets
+      // (T2D scatters class rows to strided output pixels).
+      float* stg = reinterpret_cast<float*>(wbuf);          // 32 x 36 fp32
+      int64_t* row_off = reinterpret_cast<int64_t*>(wbuf + 32 * 36 * 4);
+      const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) &&
+                          ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
+                          (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        int s, mt, g, nt;
+        decompose_tile(p, tile, s, mt, g, nt);
+        const SubProb& sp = p.sub[s];
+        {
+          const int m = mt * kBM + static_cast<int>(q * 32 + lane);
+          int64_t off = -1;
+          if (m < sp.m_count) {
+            int x = m % sp.gx, rest = m / sp.gx;
+            int y = rest % sp.gy;
+            rest /= sp.gy;
+            int z = rest % sp.gz;
+            int n = rest / sp.gz;
+            const int ox = x * sp.o_st[0] + sp.o_b[0];
+            const int oy = y * sp.o_st[1] + sp.o_b[1];
+            const int oz = z * sp.o_st[2] + sp.o_b[2];
+            const int64_t pix = ((static_cast<int64_t>(n) * p.out_dims[2] + oz) * p.out_dims[1] + oy) *
+                                    p.out_dims[0] + ox;
+            off = pix * p.ldy + g * p.cog + nt * BN;
+          }
+          row_off[lane] = off;
+        }
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+        const int ncol0 = nt * BN;
+        constexpr int kChunk = BN < 32 ? BN : 32;
+        constexpr int kLanesPerRow = kChunk / 4;
+        constexpr int kRowsPerPass = 32 / kLanesPerRow;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += kChunk) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN + c0;
+          if (kChunk == 32) tmem_ld_32x32b_x32(taddr, r);
+          else tmem_ld_32x32b_x16(taddr, r);
+          tmem_ld_wait();
+          const int valid = min(kChunk, p.cog - (ncol0 + c0));
+          if (valid <= 0) continue;  // warp-uniform
+          __syncwarp();
+          float* my = stg + lane * 36;
+#pragma unroll
+          for (int i = 0; i < kChunk; i += 4)
+            *reinterpret_cast<float4*>(my + i) = make_float4(
+                __uint_as_float(r[i]), __uint_as_float(r[i + 1]), __uint_as_float(r[i + 2]),
+                __uint_as_float(r[i + 3]));
+          __syncwarp();
+          const int col = (lane % kLanesPerRow) * 4;
+#pragma unroll 4
+          for (int rr = lane / kLanesPerRow; rr < 32; rr += kRowsPerPass) {
+            const int64_t ro = row_off[rr];
+            if (ro < 0 || col >= valid) continue;
+            const int64_t off = ro + c0 + col;
+            float4 v = *reinterpret_cast<const float4*>(stg + rr * 36 + col);
+            const bool vec = vec_ok && col + 4 <= valid;
+            if (p.accumulate) {
+              if (vec) {
+                const float4 t = *reinterpret_cast<const float4*>(p.Yin + off);
+                v.x = t.x + v.x; v.y = t.y + v.y; v.z = t.z + v.z; v.w = t.w + v.w;
+              } else {
+                float* vv = reinterpret_cast<float*>(&v);
+                for (int i = 0; i < 4 && col + i < valid; ++i) vv[i] = p.Yin[off + i] + vv[i];
+              }
+            }
+            if (p.out_f16) {
+              __half* y = reinterpret_cast<__half*>(p.Y) + off;
+              if (vec) {
+                __half2 h0 = __floats2half2_rn(v.x, v.y), h1 = __floats2half2_rn(v.z, v.w);
+                uint2 u;
+                u.x = *reinterpret_cast<uint32_t*>(&h0);
+                u.y = *reinterpret_cast<uint32_t*>(&h1);
+                *reinterpret_cast<uint2*>(y) = u;
+              } else {
+                const float* vv = reinterpret_cast<const float*>(&v);
+                for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = __float2half_rn(vv[i]);
+              }
+            } else {
+              float* y = reinterpret_cast<float*>(p.Y) + off;
+              if (vec) {
+                *reinterpret_cast<float4*>(y) = v;
+              } else {
+                const float* vv = reinterpret_cast<const float*>(&v);
+                for (int i = 0; i < 4 && col + i < valid; ++i) y[i] = vv[i];
+              }
+            }
+          }
+          __syncwarp();
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
     }
   }
 

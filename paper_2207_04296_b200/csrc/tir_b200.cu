@@ -229,22 +229,22 @@ cudaError_t launch_pdl(void (*kernel)(Params), int grid, int block, size_t smem,
 
 // ------------------------------------------------------------------ igemm launch
 
-template <int BN>
+template <int BN, int KS>
 int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
-  using Cfg = tb::IgemmCfg<BN>;
+  using Cfg = tb::IgemmCfg<BN, KS>;
   const DeviceInfo di = device_info();
   const int table = p.total_pieces * 16;
   const int budget = di.smem_optin - 1024 - 256 - table - Cfg::kEpiBytes;
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
   const int keys = p.groups * p.tiles_n;  // distinct B panels
-  const int res_rows = nst_max * tb::kBK;
+  const int res_rows = nst_max * Cfg::kBRows;
   const int res_bytes = res_rows * BN * 2;
   int grid = std::min(p.total_tiles, di.sms);
-  // Keep B resident when its whole K panel fits next to a >= 4-deep A ring and
+  // Keep B resident when its whole K panel fits next to a >= 3-deep A ring and
   // every CTA can be pinned to one (group, n-tile): grid a multiple of `keys`.
   if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && keys <= di.sms &&
-      res_rows * Cfg::kBRowBytes < (1 << 18) && res_bytes + 4 * Cfg::kABytes <= budget) {
+      res_rows * Cfg::kBRowBytes < (1 << 18) && res_bytes + 3 * Cfg::kABytes <= budget) {
     p.b_mode = tb::B_RESIDENT;
     p.b_res_rows = res_rows;
     p.stages = std::min(8, (budget - res_bytes) / Cfg::kABytes);
@@ -255,25 +255,86 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
   const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces);
-  CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
+  CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
   if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
   p.trace = g_trace;
-  tb::igemm_tc_kernel<BN><<<grid, tb::kThreads, smem, stream>>>(p);
-  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS>, grid, tb::kThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
 }
 
-int launch_igemm(tb::IgemmParams& p, int bn, cudaStream_t stream) {
+template <int BN>
+int launch_igemm_ks(tb::IgemmParams& p, int ks, cudaStream_t stream) {
+  switch (ks) {
+    case 4: return launch_igemm_bn<BN, 4>(p, stream);
+    case 2: return launch_igemm_bn<BN, 2>(p, stream);
+    default: return launch_igemm_bn<BN, 1>(p, stream);
+  }
+}
+
+int launch_igemm(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
   switch (bn) {
-    case 16: return launch_igemm_bn<16>(p, stream);
-    case 32: return launch_igemm_bn<32>(p, stream);
-    case 64: return launch_igemm_bn<64>(p, stream);
-    case 128: return launch_igemm_bn<128>(p, stream);
-    case 256: return launch_igemm_bn<256>(p, stream);
+    case 16: return launch_igemm_ks<16>(p, ks, stream);
+    case 32: return launch_igemm_ks<32>(p, ks, stream);
+    case 64: return launch_igemm_ks<64>(p, ks, stream);
+    case 128: return launch_igemm_ks<128>(p, std::min(ks, 2), stream);
+    case 256: return launch_igemm_ks<256>(p, std::min(ks, 2), stream);
   }
   return set_err(TIR_B200_ERR_UNSUPPORTED, "no kernel for BN=%d", bn);
+}
+
+// K sub-blocks (64 deep) per pipeline stage: the largest of {4, 2, 1} whose
+// padding waste (pieces past the end of the reduction) is minimal, capped by
+// shared memory (two stages of A + B must fit).
+int choose_ks(int max_pieces, int box, int bn) {
+  if (const char* e = getenv("TIR_B200_KS")) return std::max(1, std::min(4, atoi(e)));
+  const int pps1 = tb::kBK / box;
+  int best = 1;
+  int64_t best_waste = -1;
+  for (int ks : {4, 2, 1}) {
+    if (2 * ks * (16384 + 64 * bn * 2) > 190 * 1024) continue;  // two stages must fit
+    const int64_t per = static_cast<int64_t>(pps1) * ks;
+    const int64_t waste = (max_pieces + per - 1) / per * per - max_pieces;
+    if (waste * 8 <= max_pieces) return ks;  // <= 12.5% padded MMA work: deepest such stage
+    if (best_waste < 0 || waste < best_waste) {
+      best = ks;
+      best_waste = waste;
+    }
+  }
+  return best;
+}
+
+// Y as a 2-D [rows, ldy] map for the per-warp TMA-store epilogue.
+int encode_y(tb::IgemmParams& p, void* Y, int64_t rows, int out_f16) {
+  const Driver* d = driver();
+  if (!d->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  const int esz = out_f16 ? 2 : 4;
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.ldy), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldy) * esz};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = d->tiled(&p.tmY, out_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                        Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        out_f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "Y tensor map failed (%d)", (int)r);
+  return TIR_B200_OK;
+}
+
+// Store mode for row-linear outputs: TMA store when every 32-column chunk lies
+// inside one group (or there is a single group), reduce-add for in-place
+// accumulate; otherwise the generic per-row path.
+int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64_t rows, int accumulate,
+                    int out_f16) {
+  p.store_mode = 0;
+  if (getenv("TIR_B200_NO_TMA_STORE")) return TIR_B200_OK;
+  if (bn < 32 || !(p.groups == 1 || p.cog % 32 == 0) || (accumulate && Yin != Y)) return TIR_B200_OK;
+  if ((reinterpret_cast<uintptr_t>(Y) & 15) || (p.ldy * (out_f16 ? 2 : 4)) % 16) return TIR_B200_OK;
+  int rc = encode_y(p, Y, rows, out_f16);
+  if (rc) return rc;
+  p.store_mode = accumulate ? 2 : 1;
+  return TIR_B200_OK;
 }
 
 // Chooses the N tile: the whole (group) width when that still gives at least
@@ -292,7 +353,7 @@ void set_sub_identity(tb::SubProb& s) {
   }
 }
 
-int finalize_tiles(tb::IgemmParams& p, int bn) {
+int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
   p.tiles_n = static_cast<int32_t>((p.cog + bn - 1) / bn);
   int64_t t = 0, pieces = 0;
   for (int i = 0; i < p.num_sub; ++i) {
@@ -302,7 +363,7 @@ int finalize_tiles(tb::IgemmParams& p, int bn) {
     s.tiles_m = (s.m_count + tb::kBM - 1) / tb::kBM;
     s.tile_begin = static_cast<int32_t>(t);
     t += static_cast<int64_t>(s.tiles_m) * p.groups * p.tiles_n;
-    const int pps = tb::kBK / p.a_box_ch;
+    const int pps = ks * (tb::kBK / p.a_box_ch);
     s.num_stages = (s.num_pieces + pps - 1) / pps;
   }
   if (t >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "too many tiles");
@@ -334,9 +395,11 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   tb::IgemmParams p;
   std::memset(&p, 0, sizeof p);
   const int bn = choose_bn(N, (M + tb::kBM - 1) / tb::kBM, 1, di.sms);
+  const int ks = choose_ks(static_cast<int>((K + 63) / 64), 64, bn);
+  const int ks_eff = bn >= 128 ? std::min(ks, 2) : ks;
   int rc = encode_2d(&p.tmA[0], A, M, K, 64, tb::kBM);
   if (rc) return rc;
-  rc = encode_2d(&p.tmB, B, K, N, std::min(bn, 64), tb::kBK);
+  rc = encode_2d(&p.tmB, B, K, N, std::min(bn, 64), tb::kBK * ks_eff);
   if (rc) return rc;
   p.num_sub = 1;
   tb::SubProb& s = p.sub[0];
@@ -361,9 +424,11 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   p.out_f16 = out_f16;
   p.Y = C;
   p.Yin = Cin;
-  rc = finalize_tiles(p, bn);
+  rc = finalize_tiles(p, bn, ks_eff);
   if (rc) return rc;
-  return launch_igemm(p, bn, stream);
+  rc = pick_store_mode(p, bn, C, Cin, M, accumulate, out_f16);
+  if (rc) return rc;
+  return launch_igemm(p, bn, ks_eff, stream);
 }
 
 // ------------------------------------------------------------------ conv (tensor cores)
@@ -669,11 +734,15 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, box);
     if (rc) return rc;
     const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, di.sms);
-    rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK);
+    int ks = choose_ks(s.num_pieces, box, bn);
+    if (bn >= 128) ks = std::min(ks, 2);
+    rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK * ks);
     if (rc) return rc;
-    rc = finalize_tiles(p, bn);
+    rc = finalize_tiles(p, bn, ks);
     if (rc) return rc;
-    return launch_igemm(p, bn, stream);
+    rc = pick_store_mode(p, bn, Y, Yin, M, accumulate, out_f16);
+    if (rc) return rc;
+    return launch_igemm(p, bn, ks, stream);
   }
 
   // Transposed (T2D): sub-pixel decomposition into prod(s) stride-1 convs, one
@@ -740,19 +809,76 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   p.num_sub = ns;
   if (ns == 0) return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: no output classes");
   const int bn = choose_bn(cog, (m_max + tb::kBM - 1) / tb::kBM * ns, 1, di.sms);
+  int max_pieces = 0;
+  for (int i = 0; i < ns; ++i) max_pieces = std::max(max_pieces, p.sub[i].num_pieces);
+  int ks = choose_ks(max_pieces, box, bn);
+  if (bn >= 128) ks = std::min(ks, 2);
   int rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), box);
   if (rc) return rc;
-  rc = finalize_tiles(p, bn);
+  rc = finalize_tiles(p, bn, ks);
   if (rc) return rc;
-  return launch_igemm(p, bn, stream);
+  p.store_mode = 0;  // class rows scatter to strided output pixels
+  return launch_igemm(p, bn, ks, stream);
 }
 
 // ------------------------------------------------------------------ DEP
+
+template <int K, int S>
+int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
+                    int accumulate, int out_f16, cudaStream_t stream) {
+  constexpr int R = 4, T = 2, TR = 8, TC = 32;
+  constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;
+  tb::DepTileParams p;
+  std::memset(&p, 0, sizeof p);
+  const Driver* drv = driver();
+  if (!drv->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.ci), static_cast<cuuint64_t>(g.in[2]),
+                        static_cast<cuuint64_t>(g.in[1]), static_cast<cuuint64_t>(g.n)};
+  cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.ci * 2), static_cast<cuuint64_t>(g.ci * 2 * g.in[2]),
+                           static_cast<cuuint64_t>(g.ci * 2 * g.in[2] * g.in[1])};
+  cuuint32_t box[4] = {32, FC, FR, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = drv->tiled(&p.tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 4, const_cast<uint16_t*>(X), dims,
+                          strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "DEP tensor map failed (%d)", (int)r);
+  p.W = reinterpret_cast<const __half*>(W);
+  p.Yin = Yin;
+  p.Y = Y;
+  p.n = static_cast<int32_t>(g.n);
+  p.c = static_cast<int32_t>(g.ci);
+  p.oh = static_cast<int32_t>(g.out[1]);
+  p.ow = static_cast<int32_t>(g.out[2]);
+  p.pad_h = static_cast<int32_t>(g.p[1]);
+  p.pad_w = static_cast<int32_t>(g.p[2]);
+  p.tiles_h = static_cast<int32_t>((g.out[1] + TR - 1) / TR);
+  p.tiles_w = static_cast<int32_t>((g.out[2] + TC - 1) / TC);
+  p.cblocks = static_cast<int32_t>(g.ci / 32);
+  p.accumulate = accumulate;
+  p.out_f16 = out_f16;
+  const int64_t blocks = g.n * p.tiles_h * p.tiles_w * p.cblocks;
+  if (blocks >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many tiles");
+  const size_t smem = static_cast<size_t>(FR) * FC * 32 * 2;
+  auto kern = tb::dep_tile_kernel<K, S, R, T, TR, TC>;
+  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CUDA_TRY(launch_pdl(kern, static_cast<int>(blocks), 128, smem, stream, p));
+  ++g_launches;
+  return TIR_B200_OK;
+}
 
 int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
              int accumulate, int out_f16, cudaStream_t stream) {
   if (g.in[0] != 1 || g.k[0] != 1)
     return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: 2-D (NHWC) depthwise only");
+  // Fast path: 3x3, stride 1 or 2, no dilation, 32-channel blocks, aligned operands.
+  const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0) &&
+                       (!accumulate || reinterpret_cast<uintptr_t>(Yin) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(X) % 16 == 0);
+  if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 32 == 0 && g.k[1] == 3 && g.k[2] == 3 &&
+      g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
+    return g.s[1] == 1 ? launch_dep_tile<3, 1>(g, X, W, Yin, Y, accumulate, out_f16, stream)
+                       : launch_dep_tile<3, 2>(g, X, W, Yin, Y, accumulate, out_f16, stream);
+  }
   tb::DepParams p;
   p.X = reinterpret_cast<const __half*>(X);
   p.W = reinterpret_cast<const __half*>(W);
