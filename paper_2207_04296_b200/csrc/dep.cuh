@@ -153,11 +153,31 @@ __global__ void __launch_bounds__(256) dep_kernel(const DepParams p) {
 // reference's select(in-bounds, x, 0.0) padding (the oracle then adds 0*w, and
 // so does this kernel — bit-identical, including signed zeros).
 // Thread = R x T output pixels x 8 channels with all K*K*8 weights in
-// registers. It walks its input footprint ONCE in row-major order and adds
+// registers. Math: the product of two fp16 values has <= 22 significant bits,
+// so it is exact in fp32 and fma(x, w, acc) == acc + (x * w) rounded once —
+// bit-identical to the reference's separately rounded mul then add
+// (interp.cc:484-512). That lets us use packed fma.rn.f32x2 (FFMA2). It walks its input footprint ONCE in row-major order and adds
 // x * w[iy - r*S][ix - t*S] to every output that uses that pixel: for a fixed
 // output, row-major (iy, ix) visits taps in row-major (rh, rw) order — the
 // reference's reduction order — so results are bit-exact for any input.
 // Smem reads per output: (R-1)S+K)((T-1)S+K)/(R*T) instead of K*K.
+__device__ __forceinline__ uint64_t pack_f32x2(float2 v) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 unpack_f32x2(uint64_t r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+// d = a * b + c per lane, one rounding (exact product for fp16 inputs, see above)
+__device__ __forceinline__ uint64_t fma_f32x2(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 struct DepTileParams {
   CUtensorMap tmX;  // 4-D over X[N, H, W, C]: box {32, FC, FR, 1}
   const __half* W;
@@ -169,123 +189,150 @@ struct DepTileParams {
 };
 
 template <int K, int S, int R, int T, int TR, int TC>
-__global__ void __launch_bounds__(128) dep_tile_kernel(const __grid_constant__ DepTileParams p) {
+__global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant__ DepTileParams p) {
   constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;  // block footprint
   constexpr int fr = (R - 1) * S + K, fc = (T - 1) * S + K;    // thread footprint
   constexpr int CT = 32;
+  static_assert(TR == (128 / (4 * (TC / T))) * R, "128 threads = 4 channel vectors x TC/T cols x TR/R rows");
+  constexpr uint32_t kTileBytes = FR * FC * CT * 2;
+  // Persistent: the block walks tiles b, b + grid, ... with a two-slot TMA ring,
+  // so the next tile's input streams in while this one is computed and stored.
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  __half* tile = reinterpret_cast<__half*>(smem_raw);
-  __shared__ __align__(8) uint64_t bar;
+  __shared__ __align__(8) uint64_t bar[2];
+  const int tiles = p.n * p.tiles_h * p.tiles_w * p.cblocks;
 
-  int b = blockIdx.x;
-  const int cb = b % p.cblocks;
-  b /= p.cblocks;
-  const int tw = b % p.tiles_w;
-  b /= p.tiles_w;
-  const int th = b % p.tiles_h;
-  const int n = b / p.tiles_h;
-  const int oy0 = th * TR, ox0 = tw * TC, c0 = cb * CT;
+  auto tile_coords = [&](int t, int& n, int& oy0, int& ox0, int& c0) {
+    const int cb = t % p.cblocks;
+    t /= p.cblocks;
+    const int tw = t % p.tiles_w;
+    t /= p.tiles_w;
+    const int th = t % p.tiles_h;
+    n = t / p.tiles_h;
+    oy0 = th * TR;
+    ox0 = tw * TC;
+    c0 = cb * CT;
+  };
+  auto issue = [&](int t, int slot) {
+    int n, oy0, ox0, c0;
+    tile_coords(t, n, oy0, ox0, c0);
+    mbar_arrive_expect_tx(&bar[slot], kTileBytes);
+    tma_load_4d(smem_raw + slot * kTileBytes, &p.tmX, &bar[slot], c0, ox0 * S - p.pad_w,
+                oy0 * S - p.pad_h, n);
+  };
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
     fence_barrier_init();
   }
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();
-  if (threadIdx.x == 0) {
-    mbar_arrive_expect_tx(&bar, FR * FC * CT * 2);
-    tma_load_4d(tile, &p.tmX, &bar, c0, ox0 * S - p.pad_w, oy0 * S - p.pad_h, n);
+  if (threadIdx.x == 0) {  // prime both ring slots
+    if (static_cast<int>(blockIdx.x) < tiles) issue(blockIdx.x, 0);
+    if (static_cast<int>(blockIdx.x + gridDim.x) < tiles) issue(blockIdx.x + gridDim.x, 1);
   }
+
   const int cv = threadIdx.x % 4;               // 8-channel vector
   const int tc = (threadIdx.x / 4) % (TC / T);  // thread column
   const int tr = threadIdx.x / (4 * (TC / T));  // thread row
-  // weights -> registers while the tile is in flight
-  float w[K][K][8];
+  int cur_c0 = -1;
+  uint64_t w[K][K][4];  // packed fp32 pairs
+  uint32_t phase0 = 0, phase1 = 0;
+  int k = 0;
+  for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++k) {
+    const int slot = k & 1;
+    int n, oy0, ox0, c0;
+    tile_coords(t, n, oy0, ox0, c0);
+    if (c0 != cur_c0) {  // weights -> registers (once per channel block)
+      cur_c0 = c0;
 #pragma unroll
-  for (int rh = 0; rh < K; ++rh)
+      for (int rh = 0; rh < K; ++rh)
 #pragma unroll
-    for (int rw = 0; rw < K; ++rw) {
-      const uint4 u = __ldg(reinterpret_cast<const uint4*>(p.W + (rh * K + rw) * p.c + c0 + cv * 8));
-      const __half2* h = reinterpret_cast<const __half2*>(&u);
+        for (int rw = 0; rw < K; ++rw) {
+          const uint4 u = __ldg(reinterpret_cast<const uint4*>(p.W + (rh * K + rw) * p.c + c0 + cv * 8));
+          const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const float2 f = __half22float2(h[v]);
-        w[rh][rw][2 * v] = f.x;
-        w[rh][rw][2 * v + 1] = f.y;
-      }
+          for (int v = 0; v < 4; ++v) w[rh][rw][v] = pack_f32x2(__half22float2(h[v]));
+        }
     }
-  float acc[R][T][8];
+    uint64_t acc[R][T][4];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + t;
-      const bool in = oy < p.oh && ox < p.ow;
-      if (p.accumulate && in) {
-        const float* yin = p.Yin + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
-        const float4 a = *reinterpret_cast<const float4*>(yin);
-        const float4 bb = *reinterpret_cast<const float4*>(yin + 4);
-        acc[r][t][0] = a.x; acc[r][t][1] = a.y; acc[r][t][2] = a.z; acc[r][t][3] = a.w;
-        acc[r][t][4] = bb.x; acc[r][t][5] = bb.y; acc[r][t][6] = bb.z; acc[r][t][7] = bb.w;
-      } else {
+      for (int tt = 0; tt < T; ++tt) {
+        const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + tt;
+        if (p.accumulate && oy < p.oh && ox < p.ow) {
+          const float* yin = p.Yin + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
+          const float4 a = *reinterpret_cast<const float4*>(yin);
+          const float4 bb = *reinterpret_cast<const float4*>(yin + 4);
+          acc[r][tt][0] = pack_f32x2(make_float2(a.x, a.y));
+          acc[r][tt][1] = pack_f32x2(make_float2(a.z, a.w));
+          acc[r][tt][2] = pack_f32x2(make_float2(bb.x, bb.y));
+          acc[r][tt][3] = pack_f32x2(make_float2(bb.z, bb.w));
+        } else {
 #pragma unroll
-        for (int v = 0; v < 8; ++v) acc[r][t][v] = 0.0f;
+          for (int v = 0; v < 4; ++v) acc[r][tt][v] = 0ull;  // +0.0f, +0.0f
+        }
       }
-    }
-  mbar_wait(&bar, 0);
-  const __half* my = tile + ((tr * R * S) * FC + tc * T * S) * CT + cv * 8;
+    if (slot == 0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; }
+    else { mbar_wait(&bar[1], phase1); phase1 ^= 1; }
+    const __half* tile = reinterpret_cast<const __half*>(smem_raw + slot * kTileBytes);
+    const __half* my = tile + ((tr * R * S) * FC + tc * T * S) * CT + cv * 8;
 #pragma unroll
-  for (int iy = 0; iy < fr; ++iy) {
+    for (int iy = 0; iy < fr; ++iy) {
 #pragma unroll
-    for (int ix = 0; ix < fc; ++ix) {
-      const uint4 u = *reinterpret_cast<const uint4*>(my + (iy * FC + ix) * CT);
-      const __half2* h = reinterpret_cast<const __half2*>(&u);
-      float x[8];
+      for (int ix = 0; ix < fc; ++ix) {
+        const uint4 u = *reinterpret_cast<const uint4*>(my + (iy * FC + ix) * CT);
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+        uint64_t x[4];
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const float2 f = __half22float2(h[v]);
-        x[2 * v] = f.x;
-        x[2 * v + 1] = f.y;
-      }
+        for (int v = 0; v < 4; ++v) x[v] = pack_f32x2(__half22float2(h[v]));
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int rh = iy - r * S;
-        if (rh < 0 || rh >= K) continue;
+        for (int r = 0; r < R; ++r) {
+          const int rh = iy - r * S;
+          if (rh < 0 || rh >= K) continue;
 #pragma unroll
-        for (int t = 0; t < T; ++t) {
-          const int rw = ix - t * S;
-          if (rw < 0 || rw >= K) continue;
+          for (int tt = 0; tt < T; ++tt) {
+            const int rw = ix - tt * S;
+            if (rw < 0 || rw >= K) continue;
 #pragma unroll
-          for (int v = 0; v < 8; ++v)
-            acc[r][t][v] = __fadd_rn(acc[r][t][v], __fmul_rn(x[v], w[rh][rw][v]));
+            for (int v = 0; v < 4; ++v) acc[r][tt][v] = fma_f32x2(x[v], w[rh][rw][v], acc[r][tt][v]);
+          }
         }
       }
     }
-  }
+    // every thread is done reading this slot: refill it with tile k + 2
+    __syncthreads();
+    if (threadIdx.x == 0 && t + 2 * static_cast<int>(gridDim.x) < tiles)
+      issue(t + 2 * gridDim.x, slot);
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int t = 0; t < T; ++t) {
-      const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + t;
-      if (oy >= p.oh || ox >= p.ow) continue;
-      const int64_t off = ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
-      if (p.out_f16) {
-        uint4 u;
-        __half2 hh[4];
+      for (int tt = 0; tt < T; ++tt) {
+        const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + tt;
+        if (oy >= p.oh || ox >= p.ow) continue;
+        const int64_t off = ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
+        float2 f[4];
 #pragma unroll
-        for (int v = 0; v < 4; ++v) hh[v] = __floats2half2_rn(acc[r][t][2 * v], acc[r][t][2 * v + 1]);
-        u.x = *reinterpret_cast<uint32_t*>(&hh[0]);
-        u.y = *reinterpret_cast<uint32_t*>(&hh[1]);
-        u.z = *reinterpret_cast<uint32_t*>(&hh[2]);
-        u.w = *reinterpret_cast<uint32_t*>(&hh[3]);
-        *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.Y) + off) = u;
-      } else {
-        float* y = reinterpret_cast<float*>(p.Y) + off;
-        reinterpret_cast<float4*>(y)[0] = make_float4(acc[r][t][0], acc[r][t][1], acc[r][t][2], acc[r][t][3]);
-        reinterpret_cast<float4*>(y)[1] = make_float4(acc[r][t][4], acc[r][t][5], acc[r][t][6], acc[r][t][7]);
+        for (int v = 0; v < 4; ++v) f[v] = unpack_f32x2(acc[r][tt][v]);
+        if (p.out_f16) {
+          uint4 u;
+          __half2 hh[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) hh[v] = __floats2half2_rn(f[v].x, f[v].y);
+          u.x = *reinterpret_cast<uint32_t*>(&hh[0]);
+          u.y = *reinterpret_cast<uint32_t*>(&hh[1]);
+          u.z = *reinterpret_cast<uint32_t*>(&hh[2]);
+          u.w = *reinterpret_cast<uint32_t*>(&hh[3]);
+          *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.Y) + off) = u;
+        } else {
+          float* y = reinterpret_cast<float*>(p.Y) + off;
+          reinterpret_cast<float4*>(y)[0] = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
+          reinterpret_cast<float4*>(y)[1] = make_float4(f[2].x, f[2].y, f[3].x, f[3].y);
+        }
       }
-    }
+  }
 }
 
 }  // namespace tb

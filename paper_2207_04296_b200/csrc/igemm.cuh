@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
-      mbar_init(&full[i], 1);
+      mbar_init(&full[i], kProducers);  // every producer arrives once per stage
       mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
@@ -225,19 +225,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp >= 4 && warp < 4 + kProducers) {
     // ------------------------------------------------------------ producers
     pdl_wait();  // operands may be produced by the preceding kernel
+    // Every producer walks every stage and issues a round-robin share of its
+    // TMA requests (pieces j = pw mod 4; B chunks after them), arriving on the
+    // stage's full barrier with its own expect_tx. A single issuing thread
+    // completes about one request per ~500 cycles (tools/tmabw.cu), so a stage's
+    // requests are spread over four issuers.
     const int pw = static_cast<int>(warp) - 4;
-    // At most S producers: a producer's consecutive stages it and it + nprod hit
-    // slots at most one phase apart only if nprod <= S (mbarrier parity is 1 bit).
-    const int nprod = S < kProducers ? S : kProducers;
     const int box = p.a_box_ch;
     const int pps = KS * (kBK / box);  // pieces per stage
     const uint32_t piece_bytes = kBM * box * 2;
     const int a_mode = p.a_mode;
     const int b_mode = p.b_mode;
-    const uint32_t stage_tx = Cfg::kABytes + (b_mode == B_RESIDENT ? 0u : Cfg::kBBytes);
+    constexpr int kBChunks = BN / Cfg::kBChunk;
+    constexpr uint32_t kBChunkBytes = Cfg::kBRows * Cfg::kBRowBytes;  // one streamed B box
+    // bytes this producer loads per stage (same for every stage)
+    uint32_t my_tx = 0;
+    for (int j = pw; j < pps; j += kProducers) my_tx += piece_bytes;
+    if (b_mode == B_PIECES)
+      for (int j = pw; j < pps; j += kProducers) my_tx += kBChunks * box * Cfg::kBRowBytes;
+    if (b_mode == B_STREAM)
+      for (int ch = 0; ch < kBChunks; ++ch)
+        if ((pps + ch) % kProducers == pw) my_tx += kBChunkBytes;
     if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
-      // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once; the
-      // stage-row boxes are spread over the producers.
+      // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once.
       int s0, mt0, g0, nt0;
       decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
       const int col0 = g0 * p.cog + nt0 * BN;
@@ -245,16 +255,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
       __syncwarp();
       if (elect_one()) {
-        for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)  // one-shot
+        for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)
 #pragma unroll
-          for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
+          for (int ch = 0; ch < kBChunks; ++ch)
             tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
                             static_cast<size_t>(r) * Cfg::kBRowBytes,
                         &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
       }
       __syncwarp();
     }
-    int it_base = 0;
+    uint32_t slot = 0, phase = 0;
+    int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
       int s, mt, g, nt;
       decompose_tile(p, tile, s, mt, g, nt);
@@ -273,20 +284,15 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int npieces = sp.num_pieces, nst = sp.num_stages;
       const int cbase = g * p.cig;
       const int4* ptab = pieces + sp.piece_begin;
-      // producer pw owns global stages it = pw (mod nprod), so its consecutive
-      // stages are exactly nprod apart even across tile boundaries
-      const int st0 = ((pw - it_base) % nprod + nprod) % nprod;
-      for (int st = st0; pw < nprod && st < nst; st += nprod) {
-        const int it = it_base + st;
-        const uint32_t slot = static_cast<uint32_t>(it % S);
-        const uint32_t phase = static_cast<uint32_t>(it / S) & 1u;
+      for (int st = 0; st < nst; ++st, ++it) {
         mbar_wait(&empty[slot], phase ^ 1);
         if (elect_one()) {
-          if (trace && it < 128) trace[2 * it] = clock64();
+          if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();
           uint8_t* sA = sA0 + slot * Cfg::kABytes;
           uint8_t* sB = sB0 + slot * Cfg::kBBytes;
-          mbar_arrive_expect_tx(&full[slot], stage_tx);
-          for (int j = 0; j < pps; ++j) {
+          if (my_tx) mbar_arrive_expect_tx(&full[slot], my_tx);
+          else mbar_arrive(&full[slot]);
+          for (int j = pw; j < pps; j += kProducers) {
             const int pc = st * pps + j;
             void* dA = sA + j * piece_bytes;
             if (a_mode == A_TILED) {
@@ -310,22 +316,26 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             if (b_mode == B_PIECES) {
 #pragma unroll
-              for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-                tma_load_2d(sB + ch * (Cfg::kBRows * Cfg::kBRowBytes) + j * box * Cfg::kBRowBytes,
-                            &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk, e.w);
+              for (int ch = 0; ch < kBChunks; ++ch)
+                tma_load_2d(sB + ch * kBChunkBytes + j * box * Cfg::kBRowBytes, &p.tmB, &full[slot],
+                            col0 + ch * Cfg::kBChunk, e.w);
             }
           }
           if (b_mode == B_STREAM) {
 #pragma unroll
-            for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-              tma_load_2d(sB + ch * (Cfg::kBRows * Cfg::kBRowBytes), &p.tmB, &full[slot],
-                          col0 + ch * Cfg::kBChunk, st * Cfg::kBRows);
+            for (int ch = 0; ch < kBChunks; ++ch)
+              if ((pps + ch) % kProducers == pw)
+                tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk,
+                            st * Cfg::kBRows);
           }
-          if (trace && it < 128) trace[2 * it + 1] = clock64();
+          if (trace && pw == 0 && it < 128) trace[2 * it + 1] = clock64();
         }
         __syncwarp();
+        if (++slot == static_cast<uint32_t>(S)) {
+          slot = 0;
+          phase ^= 1;
+        }
       }
-      it_base += nst;
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer

@@ -826,7 +826,8 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
 template <int K, int S>
 int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
                     int accumulate, int out_f16, cudaStream_t stream) {
-  constexpr int R = 4, T = 2, TR = 8, TC = 32;
+  // 128 threads = 4 channel vectors x (TC/T) columns x (TR/R) rows
+  constexpr int R = S == 1 ? 4 : 2, T = 2, TR = 8, TC = S == 1 ? 32 : 16;
   constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;
   tb::DepTileParams p;
   std::memset(&p, 0, sizeof p);
@@ -858,10 +859,14 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   p.out_f16 = out_f16;
   const int64_t blocks = g.n * p.tiles_h * p.tiles_w * p.cblocks;
   if (blocks >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many tiles");
-  const size_t smem = static_cast<size_t>(FR) * FC * 32 * 2;
+  const size_t smem = 2 * static_cast<size_t>(FR) * FC * 32 * 2;  // two-slot ring
   auto kern = tb::dep_tile_kernel<K, S, R, T, TR, TC>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-  CUDA_TRY(launch_pdl(kern, static_cast<int>(blocks), 128, smem, stream, p));
+  int per_sm = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+  const DeviceInfo di = device_info();
+  const int grid = static_cast<int>(std::min<int64_t>(blocks, static_cast<int64_t>(std::max(per_sm, 1)) * di.sms));
+  CUDA_TRY(launch_pdl(kern, grid, 128, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
 }
