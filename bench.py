@@ -132,11 +132,30 @@ class ClockSampler:
 
 # ----------------------------------------------------------------------------- workloads
 
+# Extra tensor-bound shapes of SURVEY §8(d) (reported in `ops`, not the headline).
+EXTRA_SHAPES = {
+    "GMM8K": (8192, 8192, 8192),                     # peak demo
+    "C2D_L3": dict(op="C2D", n=16, in_dhw=(1, 14, 14), ci=256, co=256, k=(1, 3, 3), p=(0, 1, 1)),
+}
+
+
+def gmm_shape(name):
+    import paper_2207_04296_b200 as tb
+
+    return EXTRA_SHAPES[name] if name in EXTRA_SHAPES else tb.GMM_SHAPE
+
+
+def is_gmm(name):
+    return name.startswith("GMM")
+
+
 def op_spec(name):
     import paper_2207_04296_b200 as tb
 
-    if name == "GMM":
+    if is_gmm(name):
         return None
+    if name in EXTRA_SHAPES:
+        return tb.Conv(**EXTRA_SHAPES[name])
     return tb.PAPER_SHAPES[name]
 
 
@@ -145,8 +164,8 @@ def op_work(name):
     import paper_2207_04296_b200 as tb
 
     pk = peaks()
-    if name == "GMM":
-        M, N, K = tb.GMM_SHAPE
+    if is_gmm(name):
+        M, N, K = gmm_shape(name)
         flops = 2 * M * N * K
         byts = M * K * 2 + K * N * 2 + M * N * 4
     else:
@@ -170,10 +189,10 @@ class OpRunner:
         self.tb = tb
         g = torch.Generator(device=device)
         g.manual_seed(1234)
-        if name == "GMM":
-            M, N, K = tb.GMM_SHAPE
+        if is_gmm(name):
+            M, N, K = gmm_shape(name)
             set_bytes = M * K * 2 + K * N * 2 + M * N * 4
-            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
+            self.sets = min(max(2, math.ceil(2 * L2_BYTES / set_bytes)), 32)
             self.A = [torch.randn(M, K, device=device, generator=g).half() for _ in range(self.sets)]
             self.B = [torch.randn(K, N, device=device, generator=g).half() for _ in range(self.sets)]
             self.C = [torch.empty(M, N, device=device) for _ in range(self.sets)]
@@ -257,8 +276,8 @@ def measure_e2e(name, steps):
     import paper_2207_04296_b200 as tb
 
     rng = np.random.default_rng(7)
-    if name == "GMM":
-        M, N, K = tb.GMM_SHAPE
+    if is_gmm(name):
+        M, N, K = gmm_shape(name)
         A = torch.from_numpy(rng.standard_normal((M, K), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
         B = torch.from_numpy(rng.standard_normal((K, N), dtype=np.float32).astype(np.float16)).pin_memory().numpy()
         C = torch.empty((M, N), dtype=torch.float32).pin_memory().numpy()
@@ -282,7 +301,7 @@ def measure_e2e(name, steps):
     return {"value": round(flops / dt / 1e12, 4), "unit": "TFLOPS", "h2d_bytes_per_step": int(h2d),
             "d2h_bytes_per_step": int(d2h), "ms_per_step": round(dt * 1e3, 4), "steps": n,
             "timing": "host wall clock around the synchronous C-ABI host-buffer call",
-            "api": "tir_b200_conv_host" if name != "GMM" else "tir_b200_gmm_host"}
+            "api": "tir_b200_conv_host" if not is_gmm(name) else "tir_b200_gmm_host"}
 
 
 def traffic_from_profiles(name):
@@ -417,10 +436,10 @@ def main():
 
     ops = {}
     if not args.no_ops and rank == 0:
-        for other in ["GMM", "C1D", "C2D", "C3D", "DIL", "GRP", "T2D", "DEP"]:
+        for other in ["GMM", "C1D", "C2D", "C3D", "DIL", "GRP", "T2D", "DEP", "GMM8K", "C2D_L3"]:
             try:
                 r = OpRunner(other, device)
-                k = max(10, min(args.steps, 100))
+                k = max(10, min(args.steps, 100)) if other != "GMM8K" else 10
                 oms, ol, _ = time_graph(r, k, 3, None, None)
                 f, b, bd = op_work(other)
                 t = oms / 1e3 / k

@@ -97,7 +97,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], p.store_mode ? 128 : 256);
+      mbar_init(&tempty[i], p.store_mode ? 128 : 256);  // modes 1-3 use warps 0-3
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -244,6 +244,48 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       slot = nslot; phase = nphase; acc = nacc; acc_phase = nacc_phase;
     }
     (void)it_dummy;
+  } else if (p.store_mode == 3) {
+    // ------------------------------------------------------------ epilogue, 256-bit direct stores
+    // Warps 0-3: tcgen05.ld 32x32b (thread = virtual pixel) straight to
+    // st.global.v8.f32 (32 B per thread, 32 full sectors per instruction); no
+    // shared-memory traffic (the kernel's limiter is SMEM bandwidth).
+    if (warp < 4) {
+      pdl_wait();
+      const uint32_t q = warp;
+      const int m = static_cast<int>(q * 32 + lane);
+      const int ry = m / p.Wv, cx = m - ry * p.Wv;
+      uint32_t acc = 0, acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        int n, th, tw, g, nt;
+        decompose(tile, n, th, tw, g, nt);
+        const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
+        const bool ok = ry < p.R && cx < p.Wt && oy < p.oh && ox < p.ow;
+        float* yrow = reinterpret_cast<float*>(p.Y) +
+                      ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + g * p.cog + nt * BN;
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
+          tmem_ld_wait();
+          if (ok) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v)
+              asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(yrow + c0 + 8 * v),
+                           "r"(r[8 * v]), "r"(r[8 * v + 1]), "r"(r[8 * v + 2]), "r"(r[8 * v + 3]),
+                           "r"(r[8 * v + 4]), "r"(r[8 * v + 5]), "r"(r[8 * v + 6]), "r"(r[8 * v + 7])
+                           : "memory");
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
   } else if (p.store_mode) {
     // ------------------------------------------------------------ epilogue, TMA store
     // Warps 0-3 (TMEM lane quadrants; warps 4-7 idle): tcgen05.ld 32x32b (thread =

@@ -337,13 +337,28 @@ int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64
   return TIR_B200_OK;
 }
 
-// Chooses the N tile: the whole (group) width when that still gives at least
-// one wave of tiles, else the narrowest power of two >= 16 that does.
-int choose_bn(int64_t cols, int64_t m_tiles, int64_t groups, int sms) {
-  int bn = 16;
-  while (bn < cols && bn < 256) bn *= 2;
-  while (bn > 16 && m_tiles * groups * ((cols + bn - 1) / bn) < sms) bn /= 2;
-  return bn;
+// Chooses the N tile by a tensor-issue cost model measured on B200
+// (tools/mma_rate.cu): one M=128, K=16 MMA takes max(N/2, 32 + N/4) cycles
+// (SMEM operand bandwidth caps small N). Time ~ waves x k_steps x cycles/MMA,
+// with waves = ceil(tiles / SMs). A narrower tile must be >= 20% cheaper to
+// win: the model ignores the extra L2 traffic of re-reading A per N tile.
+int choose_bn(int64_t cols, int64_t m_tiles, int64_t groups, int64_t k_steps, int sms) {
+  if (const char* e = getenv("TIR_B200_BN")) return atoi(e);
+  int bn_max = 16;
+  while (bn_max < cols && bn_max < 256) bn_max *= 2;
+  int best = bn_max;
+  double best_cost = -1;
+  for (int bn = bn_max; bn >= 16; bn /= 2) {
+    const int64_t tiles = m_tiles * groups * ((cols + bn - 1) / bn);
+    const int64_t waves = (tiles + sms - 1) / sms;
+    const double cyc = std::max(bn / 2.0, 32.0 + bn / 4.0);
+    const double cost = static_cast<double>(waves) * static_cast<double>(k_steps) * cyc;
+    if (best_cost < 0 || cost < best_cost * 0.8) {
+      best = bn;
+      best_cost = cost;
+    }
+  }
+  return best;
 }
 
 void set_sub_identity(tb::SubProb& s) {
@@ -394,7 +409,7 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   const DeviceInfo di = device_info();
   tb::IgemmParams p;
   std::memset(&p, 0, sizeof p);
-  const int bn = choose_bn(N, (M + tb::kBM - 1) / tb::kBM, 1, di.sms);
+  const int bn = choose_bn(N, (M + tb::kBM - 1) / tb::kBM, 1, (K + 15) / 16, di.sms);
   const int ks = choose_ks(static_cast<int>((K + 63) / 64), 64, bn);
   const int ks_eff = bn >= 128 ? std::min(ks, 2) : ks;
   int rc = encode_2d(&p.tmA[0], A, M, K, 64, tb::kBM);
@@ -573,7 +588,7 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   p.Yin = Yin;
   // N tile: whole group width up to 256 when that still fills the machine.
   const int64_t spatial_tiles = g.n * p.tiles_h * p.tiles_w;
-  const int bn = choose_bn(cog, spatial_tiles, g.g, di.sms);
+  const int bn = choose_bn(cog, spatial_tiles, g.g, taps * (cig / 16), di.sms);
   p.tiles_n = static_cast<int32_t>((cog + bn - 1) / bn);
   const int64_t total = spatial_tiles * g.g * p.tiles_n;
   if (total >= (1ll << 31)) return kNotEligible;
@@ -608,7 +623,10 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   // updated in place (reduce-add). Otherwise direct register stores.
   p.store_mode = 0;
   p.stage_bytes = 0;
-  if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || Yin == Y) &&
+  if (getenv("TIR_B200_STORE256") && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
+      g.co % 8 == 0 && (reinterpret_cast<uintptr_t>(Y) & 31) == 0) {
+    p.store_mode = 3;
+  } else if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || Yin == Y) &&
       !getenv("TIR_B200_NO_TMA_STORE")) {
     const Driver* drv = driver();
     const int esz = out_f16 ? 2 : 4;
@@ -733,7 +751,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     p.b_mode = tb::B_STREAM;
     int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, box);
     if (rc) return rc;
-    const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, di.sms);
+    const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, taps * ((cig + 15) / 16), di.sms);
     int ks = choose_ks(s.num_pieces, box, bn);
     if (bn >= 128) ks = std::min(ks, 2);
     rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK * ks);
@@ -808,7 +826,9 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
       }
   p.num_sub = ns;
   if (ns == 0) return set_err(TIR_B200_ERR_UNSUPPORTED, "T2D: no output classes");
-  const int bn = choose_bn(cog, (m_max + tb::kBM - 1) / tb::kBM * ns, 1, di.sms);
+  int kmax = 0;
+  for (int i = 0; i < ns; ++i) kmax = std::max(kmax, p.sub[i].taps[0] * p.sub[i].taps[1] * p.sub[i].taps[2]);
+  const int bn = choose_bn(cog, (m_max + tb::kBM - 1) / tb::kBM * ns, 1, kmax * ((cig + 15) / 16), di.sms);
   int max_pieces = 0;
   for (int i = 0; i < ns; ++i) max_pieces = std::max(max_pieces, p.sub[i].num_pieces);
   int ks = choose_ks(max_pieces, box, bn);

@@ -1,7 +1,4 @@
-# A/B of epilogue modes on the C2D headline (bench only)
-for mode in default no_tma_store; do
-  if [ $mode = no_tma_store ]; then export TIR_B200_NO_TMA_STORE=1; fi
-  python bench.py --steps 200 --warmup 5 --no-cpu --no-ops --no-e2e > gpurun_out/ab_$mode.json 2>/dev/null
-  TIR_B200_NO_PDL=1 python bench.py --steps 200 --warmup 5 --no-cpu --no-ops --no-e2e > gpurun_out/ab_${mode}_nopdl.json 2>/dev/null
-done
-python tools/trace_igemm.py > gpurun_out/trace_direct.txt 2>&1
+python tests/gpu_diag.py c2d_paper > gpurun_out/ab.txt 2>&1
+TIR_B200_STORE256=1 python tests/gpu_diag.py c2d_paper halo_c2d_wide halo_c2d_co256 >> gpurun_out/ab.txt 2>&1
+python bench.py --steps 200 --warmup 5 --no-cpu --no-ops --no-e2e > gpurun_out/ab_default.json 2>/dev/null
+TIR_B200_STORE256=1 python bench.py --steps 200 --warmup 5 --no-cpu --no-ops --no-e2e > gpurun_out/ab_s256.json 2>/dev/null
