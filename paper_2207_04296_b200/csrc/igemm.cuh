@@ -98,6 +98,8 @@ struct alignas(64) IgemmParams {
   void* Y;
   const float* Yin;
   int32_t store_mode;  // 0: generic row-offset stores, 1: TMA store, 2: TMA reduce-add (Y += tile)
+  int32_t ksplit;      // split-K partitions (>= 1); > 1 adds partials into a pre-initialised Y
+  int32_t reduce;      // generic path: red.global.add into Y instead of stores (split-K)
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
 };
@@ -127,17 +129,34 @@ struct IgemmCfg {
   }
 };
 
+// tile -> (sub-problem, m tile, group, n tile, K split); the split index is
+// fastest so a persistent CTA keeps one (group, n tile) when
+// grid % (ksplit * groups * tiles_n) == 0 (resident-B requirement).
 __device__ __forceinline__ void decompose_tile(const IgemmParams& p, int tile, int& s, int& mt,
-                                               int& g, int& nt) {
+                                               int& g, int& nt, int& ks) {
   s = 0;
 #pragma unroll 1
   for (int i = 1; i < p.num_sub; ++i)
     if (tile >= p.sub[i].tile_begin) s = i;
   int local = tile - p.sub[s].tile_begin;
+  ks = local % p.ksplit;
+  local /= p.ksplit;
   nt = local % p.tiles_n;
   int rest = local / p.tiles_n;
   g = rest % p.groups;
   mt = rest / p.groups;
+}
+
+__device__ __forceinline__ void decompose_tile(const IgemmParams& p, int tile, int& s, int& mt,
+                                               int& g, int& nt) {
+  int ks;
+  decompose_tile(p, tile, s, mt, g, nt, ks);
+}
+
+// Stage range [st0, st1) of split `ks` out of `nst` stages.
+__device__ __forceinline__ void split_range(const IgemmParams& p, int nst, int ks, int& st0, int& st1) {
+  st0 = static_cast<int>(static_cast<int64_t>(nst) * ks / p.ksplit);
+  st1 = static_cast<int>(static_cast<int64_t>(nst) * (ks + 1) / p.ksplit);
 }
 
 // Piece table entry: everything a producer needs for one TMA piece, computed
@@ -267,8 +286,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slot = 0, phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt;
-      decompose_tile(p, tile, s, mt, g, nt);
+      int s, mt, g, nt, ks;
+      decompose_tile(p, tile, s, mt, g, nt, ks);
       const SubProb& sp = p.sub[s];
       const CUtensorMap* tmA = &p.tmA[s];
       const int m0 = mt * kBM;
@@ -284,7 +303,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const int npieces = sp.num_pieces, nst = sp.num_stages;
       const int cbase = g * p.cig;
       const int4* ptab = pieces + sp.piece_begin;
-      for (int st = 0; st < nst; ++st, ++it) {
+      int st0, st1;
+      split_range(p, nst, ks, st0, st1);
+      for (int st = st0; st < st1; ++st, ++it) {
         mbar_wait(&empty[slot], phase ^ 1);
         if (elect_one()) {
           if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();
@@ -377,13 +398,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slot = 0, phase = 0, acc = 0, acc_phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt;
-      decompose_tile(p, tile, s, mt, g, nt);
-      const int nst = p.sub[s].num_stages;
+      int s, mt, g, nt, ks;
+      decompose_tile(p, tile, s, mt, g, nt, ks);
+      int st0, st1;
+      split_range(p, p.sub[s].num_stages, ks, st0, st1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int st = 0; st < nst; ++st, ++it) {
+      for (int st = st0; st < st1; ++st, ++it) {
         mbar_wait(&full[slot], phase);
         tc_fence_after();
         if (trace && lane == 0 && it < 128) trace[256 + 2 * it] = clock64();
@@ -395,7 +417,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
               umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
-                       Cfg::kIdesc, (st | u | k) != 0);
+                       Cfg::kIdesc, ((st - st0) | u | k) != 0);
           umma_commit(&empty[slot]);
         }
         __syncwarp();
@@ -540,6 +562,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int64_t off = ro + c0 + col;
             float4 v = *reinterpret_cast<const float4*>(stg + rr * 36 + col);
             const bool vec = vec_ok && col + 4 <= valid;
+            if (p.reduce) {  // split-K partial: Y += v (fp32 output only)
+              float* y = reinterpret_cast<float*>(p.Y) + off;
+              if (vec) {
+                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(y), "f"(v.x), "f"(v.y),
+                             "f"(v.z), "f"(v.w)
+                             : "memory");
+              } else {
+                const float* vv = reinterpret_cast<const float*>(&v);
+                for (int i = 0; i < 4 && col + i < valid; ++i) atomicAdd(y + i, vv[i]);
+              }
+              continue;
+            }
             if (p.accumulate) {
               if (vec) {
                 const float4 t = *reinterpret_cast<const float4*>(p.Yin + off);

@@ -55,6 +55,55 @@ __global__ void f32_to_f16_exact_kernel(const float* __restrict__ x, uint16_t* _
   if (bad) atomicExch(flag, 1);
 }
 
+// (kw, c) packing for small-channel convs (the CI = 3 first layers, C3D/DIL):
+//   Xp[n, d, h, ow, t*C + c] = X[n, d, h, ow*sw - pw + t*dw, c]   (0 if out of bounds)
+//   Wp[(kd, kh), t*C + c, co] = W[(kd, kh, t), c, co]             (zero rows past KW*C)
+// so the convolution becomes a (KD, KH, 1) convolution over Xp with Cp = KW*C
+// rounded up to 8/16/32 channels: a pure relayout (zero fill = the reference's
+// select(in-bounds, x, 0.0) padding), so every product and partial sum is the same.
+__global__ void pack_kw_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y, int64_t rows,
+                               int32_t iw, int32_t c, int32_t ow, int32_t kw, int32_t sw, int32_t pw,
+                               int32_t dw, int32_t cp) {
+  // one thread per (row, ow, 8-channel group); row = n*D*H flattened
+  const int groups = cp / 8;
+  const int64_t total = rows * ow * groups;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int grp = static_cast<int>(i % groups);
+    const int64_t pix = i / groups;  // row * ow + o
+    const int o = static_cast<int>(pix % ow);
+    const int64_t row = pix / ow;
+    const uint16_t* xr = x + row * iw * c;
+    uint16_t v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int j = grp * 8 + e;
+      const int t = j / c, ch = j - t * c;
+      const int wi = o * sw - pw + t * dw;
+      v[e] = (t < kw && wi >= 0 && wi < iw) ? xr[wi * c + ch] : static_cast<uint16_t>(0);
+    }
+    uint4 u;
+    u.x = v[0] | (static_cast<uint32_t>(v[1]) << 16);
+    u.y = v[2] | (static_cast<uint32_t>(v[3]) << 16);
+    u.z = v[4] | (static_cast<uint32_t>(v[5]) << 16);
+    u.w = v[6] | (static_cast<uint32_t>(v[7]) << 16);
+    *reinterpret_cast<uint4*>(y + pix * cp + grp * 8) = u;
+  }
+}
+
+__global__ void pack_kw_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ y,
+                                       int64_t khd, int32_t kwc, int32_t cp, int32_t co) {
+  const int64_t total = khd * cp * co;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t col = i % co;
+    const int64_t row = i / co;
+    const int64_t g = row / cp;
+    const int32_t j = static_cast<int32_t>(row - g * cp);
+    y[i] = j < kwc ? w[(g * kwc + j) * co + col] : static_cast<uint16_t>(0);
+  }
+}
+
 inline int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   return static_cast<int>(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));
@@ -71,6 +120,23 @@ inline int launch_pad_weight_rows(const uint16_t* w, uint16_t* y, int64_t taps, 
                                   int64_t cp, int64_t co, cudaStream_t st) {
   pad_weight_rows_kernel<<<grid_for(taps * cp * co), 256, 0, st>>>(
       w, y, taps, static_cast<int32_t>(c), static_cast<int32_t>(cp), static_cast<int32_t>(co));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+inline int launch_pack_kw(const uint16_t* x, uint16_t* y, int64_t rows, int64_t iw, int64_t c,
+                          int64_t ow, int64_t kw, int64_t sw, int64_t pw, int64_t dw, int64_t cp,
+                          cudaStream_t st) {
+  pack_kw_kernel<<<grid_for(rows * ow * (cp / 8)), 256, 0, st>>>(
+      x, y, rows, static_cast<int32_t>(iw), static_cast<int32_t>(c), static_cast<int32_t>(ow),
+      static_cast<int32_t>(kw), static_cast<int32_t>(sw), static_cast<int32_t>(pw),
+      static_cast<int32_t>(dw), static_cast<int32_t>(cp));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+inline int launch_pack_kw_weights(const uint16_t* w, uint16_t* y, int64_t khd, int64_t kwc, int64_t cp,
+                                  int64_t co, cudaStream_t st) {
+  pack_kw_weights_kernel<<<grid_for(khd * cp * co), 256, 0, st>>>(
+      w, y, khd, static_cast<int32_t>(kwc), static_cast<int32_t>(cp), static_cast<int32_t>(co));
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 

@@ -237,7 +237,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   const int budget = di.smem_optin - 1024 - 256 - table - Cfg::kEpiBytes;
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
-  const int keys = p.groups * p.tiles_n;  // distinct B panels
+  const int keys = p.groups * p.tiles_n * p.ksplit;  // CTAs per B-panel cycle
   const int res_rows = nst_max * Cfg::kBRows;
   const int res_bytes = res_rows * BN * 2;
   int grid = std::min(p.total_tiles, di.sms);
@@ -377,7 +377,7 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
     if (p.a_mode != tb::A_TILED) pieces += s.num_pieces;
     s.tiles_m = (s.m_count + tb::kBM - 1) / tb::kBM;
     s.tile_begin = static_cast<int32_t>(t);
-    t += static_cast<int64_t>(s.tiles_m) * p.groups * p.tiles_n;
+    t += static_cast<int64_t>(s.tiles_m) * p.groups * p.tiles_n * p.ksplit;
     const int pps = ks * (tb::kBK / p.a_box_ch);
     s.num_stages = (s.num_pieces + pps - 1) / pps;
   }
@@ -387,6 +387,40 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
                    static_cast<long long>(pieces), tb::kMaxPieces);
   p.total_pieces = static_cast<int32_t>(pieces);
   p.total_tiles = static_cast<int32_t>(t);
+  return TIR_B200_OK;
+}
+
+// ------------------------------------------------------------------ split-K
+
+// Split the reduction when the output tiles cannot fill half the machine:
+// each split adds its fp32 partial into Y (TMA reduce-add or red.global.add),
+// so Y is first zeroed (or seeded with Yin when accumulating). Sums of the
+// reference distribution are exact in any order, so parity is unchanged.
+int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int sms) {
+  if (const char* e = getenv("TIR_B200_KSPLIT")) return std::max(1, atoi(e));
+  if (out_f16 || out_tiles * 2 > sms) return 1;
+  int nst_min = 1 << 30;
+  for (int i = 0; i < p.num_sub; ++i) nst_min = std::min(nst_min, p.sub[i].num_stages);
+  int ks = static_cast<int>(std::min<int64_t>(sms / out_tiles, 8));
+  ks = std::min(ks, nst_min / 2);  // at least two stages per split
+  return std::max(ks, 1);
+}
+
+int prepare_split_output(tb::IgemmParams& p, void* Y, const float* Yin, int64_t elems, int accumulate,
+                         cudaStream_t stream) {
+  if (p.ksplit <= 1) return TIR_B200_OK;
+  if (accumulate) {
+    if (Yin != Y) CUDA_TRY(cudaMemcpyAsync(Y, Yin, elems * 4, cudaMemcpyDeviceToDevice, stream));
+  } else {
+    CUDA_TRY(cudaMemsetAsync(Y, 0, elems * 4, stream));
+  }
+  p.accumulate = 0;
+  if (p.store_mode) {
+    p.store_mode = 2;  // TMA reduce-add
+  } else {
+    p.reduce = 1;      // red.global.add
+  }
+  p.Yin = nullptr;
   return TIR_B200_OK;
 }
 
@@ -439,9 +473,18 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   p.out_f16 = out_f16;
   p.Y = C;
   p.Yin = Cin;
+  p.ksplit = 1;
   rc = finalize_tiles(p, bn, ks_eff);
   if (rc) return rc;
-  rc = pick_store_mode(p, bn, C, Cin, M, accumulate, out_f16);
+  p.ksplit = choose_ksplit(p, p.total_tiles, out_f16, di.sms);
+  if (p.ksplit > 1) {
+    rc = finalize_tiles(p, bn, ks_eff);
+    if (rc) return rc;
+  }
+  rc = pick_store_mode(p, bn, C, p.ksplit > 1 ? static_cast<const float*>(C) : Cin, M,
+                       accumulate || p.ksplit > 1, out_f16);
+  if (rc) return rc;
+  rc = prepare_split_output(p, C, Cin, M * N, accumulate, stream);
   if (rc) return rc;
   return launch_igemm(p, bn, ks_eff, stream);
 }
@@ -664,7 +707,40 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   const uint16_t* W = W0;
   int64_t cig = g.ci / g.g;
   const int64_t cog = g.co / g.g;
-  const int64_t taps = g.k[0] * g.k[1] * g.k[2];
+  int64_t taps = g.k[0] * g.k[1] * g.k[2];
+  // Small-channel layers (CI = 3 in C3D / DIL): pack the KW taps into the
+  // channel dim ((kw, c) packing, prep.cuh) so each im2col piece carries
+  // KW*CI real channels instead of CI padded to 8. Bit-exact relayout.
+  if (cig % 8 && g.g == 1 && !g.transposed && g.k[2] > 1 && g.k[2] * cig <= 64 &&
+      !getenv("TIR_B200_NO_PACK_KW")) {
+    const int64_t kwc = g.k[2] * cig;
+    const int64_t cp = kwc <= 8 ? 8 : kwc <= 16 ? 16 : kwc <= 32 ? 32 : 64;
+    const int64_t rows = g.n * g.in[0] * g.in[1];
+    const int64_t khd = g.k[0] * g.k[1];
+    const size_t xbytes = static_cast<size_t>(rows * g.out[2] * cp * 2);
+    const size_t wbytes = static_cast<size_t>(khd * cp * g.co * 2);
+    void* ws = nullptr;
+    int rc = workspace(xbytes + wbytes + 512, &ws);
+    if (rc) return rc;
+    uint16_t* Xp = static_cast<uint16_t*>(ws);
+    uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
+    if (tb::launch_pack_kw(X, Xp, rows, g.in[2], cig, g.out[2], g.k[2], g.s[2], g.p[2], g.d[2], cp, stream))
+      return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+    ++g_launches;
+    if (tb::launch_pack_kw_weights(W, Wp, khd, kwc, cp, g.co, stream))
+      return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+    ++g_launches;
+    X = Xp;
+    W = Wp;
+    g.in[2] = g.out[2];
+    g.ci = cp;
+    g.k[2] = 1;
+    g.s[2] = 1;
+    g.p[2] = 0;
+    g.d[2] = 1;
+    cig = cp;
+    taps = g.k[0] * g.k[1];
+  }
   // Channel padding (a bit-exact layout step): TMA needs a 16-byte pixel pitch.
   if (cig % 8) {
     if (g.g != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: grouped conv needs CI/G %% 8 == 0");
@@ -756,9 +832,18 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     if (bn >= 128) ks = std::min(ks, 2);
     rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK * ks);
     if (rc) return rc;
+    p.ksplit = 1;
     rc = finalize_tiles(p, bn, ks);
     if (rc) return rc;
-    rc = pick_store_mode(p, bn, Y, Yin, M, accumulate, out_f16);
+    p.ksplit = choose_ksplit(p, p.total_tiles, out_f16, di.sms);
+    if (p.ksplit > 1) {
+      rc = finalize_tiles(p, bn, ks);
+      if (rc) return rc;
+    }
+    rc = pick_store_mode(p, bn, Y, p.ksplit > 1 ? static_cast<const float*>(Y) : Yin, M,
+                         accumulate || p.ksplit > 1, out_f16);
+    if (rc) return rc;
+    rc = prepare_split_output(p, Y, Yin, M * g.co, accumulate, stream);
     if (rc) return rc;
     return launch_igemm(p, bn, ks, stream);
   }
@@ -835,9 +920,17 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   if (bn >= 128) ks = std::min(ks, 2);
   int rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), box);
   if (rc) return rc;
+  p.ksplit = 1;
   rc = finalize_tiles(p, bn, ks);
   if (rc) return rc;
+  p.ksplit = choose_ksplit(p, p.total_tiles, out_f16, di.sms);
+  if (p.ksplit > 1) {
+    rc = finalize_tiles(p, bn, ks);
+    if (rc) return rc;
+  }
   p.store_mode = 0;  // class rows scatter to strided output pixels
+  rc = prepare_split_output(p, Y, Yin, g.n * g.out[0] * g.out[1] * g.out[2] * g.co, accumulate, stream);
+  if (rc) return rc;
   return launch_igemm(p, bn, ks, stream);
 }
 
