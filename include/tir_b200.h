@@ -72,6 +72,16 @@ typedef struct {
   int64_t groups;
 } tir_b200_conv_desc;
 
+/* Fused epilogue, applied per output element after the
+ * reduction, in this order:  v = acc;  v = Yin + v (accumulate);  v = v + bias[col];
+ * v = max(v, 0) (relu). `bias` is fp32 per output column (GMM: N, conv: CO);
+ * either field may be 0/NULL. gemm + relu is the reference's gemm_relu_source
+ * workload (tests/testing/workloads.h:61-91) as one intrinsic. */
+typedef struct {
+  const float* bias;
+  int32_t relu;
+} tir_b200_epilogue;
+
 /* Library / device facts. */
 int tir_b200_version(void);
 const char* tir_b200_last_error(void);
@@ -92,6 +102,15 @@ int tir_b200_gmm(const uint16_t* A, const uint16_t* B, const float* Cin, void* C
 
 int tir_b200_conv(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
                   const float* Yin, void* Y, int accumulate, int out_f16, void* stream);
+
+/* The same with a fused epilogue (epi may be NULL). */
+int tir_b200_gmm_ex(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
+                    int64_t N, int64_t K, int accumulate, int out_f16, const tir_b200_epilogue* epi,
+                    void* stream);
+
+int tir_b200_conv_ex(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                     const float* Yin, void* Y, int accumulate, int out_f16,
+                     const tir_b200_epilogue* epi, void* stream);
 
 /* ---- host-buffer entry points (synchronous; H2D, compute, D2H) ----
  * These are what the reference-side HostKernel adapter calls: operands live in

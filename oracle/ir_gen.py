@@ -290,6 +290,43 @@ def tensorized_conv_source(spec: ConvSpec, intrin: str, name: str = "conv_t") ->
     )
 
 
+def with_epilogue(src: str, out_shape: tuple, bias: bool = False, relu: bool = False) -> str:
+    """Adds the fused-epilogue stage to a contraction program:
+    the output C becomes an `alloc` intermediate and a second nest writes
+    D = max(C + Bias[last dim], 0.0) — the shape of the reference's own
+    gemm_relu_source (tests/testing/workloads.h:61-91: alloc C, then
+    `D[vi, vj] = max(C[vi, vj], 0.0)`), generalised with an optional f32 bias
+    per output column. Inputs become (A, B[, Bias]); the output is D."""
+    dims = _dims(None, out_shape)
+    head = f"C: f32[{dims}]) {{\n  block root() {{\n"
+    if src.count(head) != 1:
+        raise ValueError("program does not have the expected C output signature")
+    params = (f"Bias: f32[{out_shape[-1]}], " if bias else "") + f"D: f32[{dims}]"
+    src = src.replace(head, f"{params}) {{\n  block root() {{\n    alloc C: f32[{dims}]\n")
+    tail = "  }\n}\n"
+    assert src.endswith(tail)
+    body = src[: -len(tail)]
+    nd = len(out_shape)
+    ind = "  "
+    lines = []
+    for i, e in enumerate(out_shape):
+        lines.append(ind * (2 + i) + f"for e{i} in 0..{e} {{")
+    binds = ", ".join(f"spatial u{i}: {e} = e{i}" for i, e in enumerate(out_shape))
+    idx = ", ".join(f"u{i}" for i in range(nd))
+    reg = ", ".join(f"u{i} +: 1" for i in range(nd))
+    reads = f"C[{reg}]" + (f", Bias[u{nd - 1} +: 1]" if bias else "")
+    val = f"C[{idx}]" + (f" + Bias[u{nd - 1}]" if bias else "")
+    if relu:
+        val = f"max({val}, 0.0)"
+    d = ind * (2 + nd)
+    lines.append(d + f"block epi({binds}) reads({reads}) writes(D[{reg}]) {{")
+    lines.append(d + f"  D[{idx}] = {val}")
+    lines.append(d + "}")
+    for i in reversed(range(nd)):
+        lines.append(ind * (2 + i) + "}")
+    return body + "\n".join(lines) + "\n" + tail
+
+
 # ---- the paper's single-op suite (SURVEY §8(d) proposed benchmark shapes) ----
 
 PAPER_SHAPES = {

@@ -203,6 +203,19 @@ def conv(spec: ConvSpec, X: np.ndarray, W: np.ndarray, Y: np.ndarray | None = No
     return out
 
 
+def epilogue(Y: np.ndarray, bias: np.ndarray | None = None, relu: bool = False) -> np.ndarray:
+    """Fused-epilogue stage in f32: Y + bias[last dim], then max(v, 0.0) as the
+    interpreter evaluates max (std::max, interp.cc:499; the relu block of
+    gemm_relu_source, tests/testing/workloads.h:83-88). NaN / -0.0 pass through
+    like std::max(v, 0.0) = (v < 0) ? 0 : v."""
+    out = np.array(Y, np.float32, copy=True)
+    if bias is not None:
+        out = (out + np.asarray(bias, np.float32)).astype(np.float32)
+    if relu:
+        out = np.where(out < 0, np.float32(0), out).astype(np.float32)
+    return out
+
+
 # ---------------- the reference interpreter (oracle/_ref) ----------------
 
 def ref_available() -> bool:

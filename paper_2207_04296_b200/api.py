@@ -97,6 +97,11 @@ class Conv:
         return replace(self, **kw)
 
 
+class Epilogue(ctypes.Structure):
+    """tir_b200_epilogue: optional per-column fp32 bias, then ReLU (include/tir_b200.h)."""
+    _fields_ = [("bias", ctypes.c_void_p), ("relu", ctypes.c_int32)]
+
+
 _lib = None
 
 
@@ -113,6 +118,9 @@ def lib() -> ctypes.CDLL:
         L.tir_b200_conv_out_shape.argtypes = [ctypes.POINTER(ConvDesc), ctypes.POINTER(i64)]
         L.tir_b200_gmm.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32, i32, vp]
         L.tir_b200_conv.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, vp, i32, i32, vp]
+        ep = ctypes.POINTER(Epilogue)
+        L.tir_b200_gmm_ex.argtypes = [vp, vp, vp, vp, i64, i64, i64, i32, i32, ep, vp]
+        L.tir_b200_conv_ex.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, vp, i32, i32, ep, vp]
         L.tir_b200_gmm_host.argtypes = [vp, vp, vp, i64, i64, i64, i32]
         L.tir_b200_conv_host.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, i32]
         L.tir_b200_gmm_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i32]
@@ -162,8 +170,22 @@ def _need(t, dtype, shape, name):
     del torch
 
 
-def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, stream=None):
+def _epilogue(bias, relu, cols, device):
+    """Builds the C-ABI epilogue; None when neither bias nor relu is requested."""
+    if bias is None and not relu:
+        return None
+    torch = _torch()
+    if bias is not None:
+        _need(bias, torch.float32, (cols,), "bias")
+        if bias.device != device:
+            raise TirError("ValueError", "bias must live on the operands' device")
+    return Epilogue(bias.data_ptr() if bias is not None else None, int(bool(relu)))
+
+
+def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, bias=None,
+        relu: bool = False, stream=None):
     """C (+)= A @ B with A [M,K] fp16, B [K,N] fp16 (N contiguous), fp32 accumulation.
+    Optional fused epilogue: C = relu((C +) A @ B + bias[N]).
     Returns C ([M,N] fp32, or fp16 if out_f16)."""
     torch = _torch()
     M, K = A.shape
@@ -177,14 +199,21 @@ def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, stream
     _need(C, torch.float16 if out_f16 else torch.float32, (M, N), "C")
     if accumulate and out_f16:
         raise TirError("ValueError", "accumulate requires an fp32 C")
-    _check(lib().tir_b200_gmm(_ptr(A), _ptr(B), _ptr(C) if accumulate else None, _ptr(C), M, N, K,
-                              int(accumulate), int(out_f16), _stream(stream)))
+    epi = _epilogue(bias, relu, N, A.device)
+    if epi is None:
+        _check(lib().tir_b200_gmm(_ptr(A), _ptr(B), _ptr(C) if accumulate else None, _ptr(C), M, N, K,
+                                  int(accumulate), int(out_f16), _stream(stream)))
+    else:
+        _check(lib().tir_b200_gmm_ex(_ptr(A), _ptr(B), _ptr(C) if accumulate else None, _ptr(C), M, N,
+                                     K, int(accumulate), int(out_f16), ctypes.byref(epi),
+                                     _stream(stream)))
     return C
 
 
 def conv(spec: Conv, X, W, Y=None, *, accumulate: bool = False, out_f16: bool = False,
-         stream=None):
-    """Y (+)= conv(X, W) for C1D/C2D/C3D/DIL/GRP/T2D/DEP (layouts: include/tir_b200.h)."""
+         bias=None, relu: bool = False, stream=None):
+    """Y (+)= conv(X, W) for C1D/C2D/C3D/DIL/GRP/T2D/DEP (layouts: include/tir_b200.h).
+    Optional fused epilogue: Y = relu((Y +) conv(X, W) + bias[CO])."""
     torch = _torch()
     _need(X, torch.float16, spec.x_shape(), "X")
     _need(W, torch.float16, spec.w_shape(), "W")
@@ -197,8 +226,14 @@ def conv(spec: Conv, X, W, Y=None, *, accumulate: bool = False, out_f16: bool = 
     if accumulate and out_f16:
         raise TirError("ValueError", "accumulate requires an fp32 Y")
     d = spec.desc()
-    _check(lib().tir_b200_conv(ctypes.byref(d), _ptr(X), _ptr(W), _ptr(Y) if accumulate else None,
-                               _ptr(Y), int(accumulate), int(out_f16), _stream(stream)))
+    epi = _epilogue(bias, relu, spec.co, X.device)
+    if epi is None:
+        _check(lib().tir_b200_conv(ctypes.byref(d), _ptr(X), _ptr(W), _ptr(Y) if accumulate else None,
+                                   _ptr(Y), int(accumulate), int(out_f16), _stream(stream)))
+    else:
+        _check(lib().tir_b200_conv_ex(ctypes.byref(d), _ptr(X), _ptr(W),
+                                      _ptr(Y) if accumulate else None, _ptr(Y), int(accumulate),
+                                      int(out_f16), ctypes.byref(epi), _stream(stream)))
     return Y
 
 

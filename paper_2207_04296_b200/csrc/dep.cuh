@@ -29,6 +29,8 @@ struct DepParams {
   int32_t n, ih, iw, c, oh, ow;
   int32_t kh, kw, sh, sw, ph, pw, dh, dw;
   int32_t accumulate, out_f16;
+  const float* bias;  // fused epilogue (nullable)
+  int32_t relu;
 };
 
 template <int VEC, int R>
@@ -114,6 +116,10 @@ __global__ void __launch_bounds__(256) dep_kernel(const DepParams p) {
       const int oy = oy0 + r;
       if (oy >= p.oh) break;
       const int64_t off = ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0;
+      if (p.bias || p.relu) {
+#pragma unroll
+        for (int v = 0; v < VEC; ++v) acc[r][v] = epi_apply(acc[r][v], p.bias, c0 + v, p.relu);
+      }
       if (p.out_f16) {
         __half* y = reinterpret_cast<__half*>(p.Y) + off;
         if constexpr (VEC == 8) {
@@ -186,9 +192,11 @@ struct DepTileParams {
   int32_t n, c, oh, ow, pad_h, pad_w;
   int32_t tiles_h, tiles_w, cblocks;
   int32_t accumulate, out_f16;
+  const float* bias;  // fused epilogue (nullable)
+  int32_t relu;
 };
 
-template <int K, int S, int R, int T, int TR, int TC>
+template <int K, int S, int R, int T, int TR, int TC, bool EPI>
 __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant__ DepTileParams p) {
   constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;  // block footprint
   constexpr int fr = (R - 1) * S + K, fc = (T - 1) * S + K;    // thread footprint
@@ -316,6 +324,13 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
         float2 f[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) f[v] = unpack_f32x2(acc[r][tt][v]);
+        if (EPI) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            f[v].x = epi_apply(f[v].x, p.bias, c0 + cv * 8 + 2 * v, p.relu);
+            f[v].y = epi_apply(f[v].y, p.bias, c0 + cv * 8 + 2 * v + 1, p.relu);
+          }
+        }
         if (p.out_f16) {
           uint4 u;
           __half2 hh[4];

@@ -48,6 +48,8 @@ struct alignas(64) HaloParams {
   int32_t stages;             // halo ring depth
   int32_t slab_rows;          // smem rows per slab (>= max tap offset + 128)
   int32_t accumulate, out_f16;
+  const float* bias;  // fused epilogue: per-output-column bias (nullable)
+  int32_t relu;       // fused epilogue: max(v, 0)
   int32_t store_mode;         // 0: direct register stores, 1: TMA store, 2: TMA reduce-add (Y += )
   int32_t nacc;               // TMEM accumulator buffers (MMA runs nacc-1 tiles ahead)
   int32_t stage_bytes;        // TMA-store staging buffer bytes (one of two)
@@ -313,6 +315,13 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
           tmem_ld_wait();
+          if (p.bias || p.relu) {
+            const int64_t colb = g * p.cog + nt * BN + c0;
+            const int lim = p.cog - (nt * BN + c0);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < lim) r[i] = __float_as_uint(epi_apply(__uint_as_float(r[i]), p.bias, colb + i, p.relu));
+          }
           uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
           named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store
           if (mine) {
@@ -415,6 +424,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
               } else {
                 v0 = p.Yin[off] + v0;
               }
+            }
+            if (p.bias || p.relu) {
+              const int64_t colb = g * p.cog + ncol0 + c0 + col;
+              v0 = epi_apply(v0, p.bias, colb, p.relu);
+              if (pair) v1 = epi_apply(v1, p.bias, colb + 1, p.relu);
             }
             if (p.out_f16) {
               __half* y = reinterpret_cast<__half*>(p.Y) + off;

@@ -91,6 +91,8 @@ struct alignas(64) IgemmParams {
   int32_t ldy;         // Y row pitch in elements (CO, or GMM N)
   int32_t out_dims[3]; // OW, OH, OD
   int32_t accumulate;
+  const float* bias;  // fused epilogue: per-output-column bias (nullable)
+  int32_t relu;       // fused epilogue: max(v, 0)
   int32_t out_f16;
   int32_t stages;      // smem ring depth
   int32_t b_res_rows;  // B_RESIDENT: rows of the resident panel (multiple of 64)
@@ -458,6 +460,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
           tmem_ld_wait();
           if (nt * BN + c0 >= p.cog) continue;  // warp-uniform: chunk past the group
+          if (p.bias || p.relu) {
+            const int64_t colb = g * p.cog + nt * BN + c0;
+            const int lim = p.cog - (nt * BN + c0);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < lim) r[i] = __float_as_uint(epi_apply(__uint_as_float(r[i]), p.bias, colb + i, p.relu));
+          }
           uint8_t* buf = wbuf + (chunk & 1) * 4096;
           __syncwarp();  // lane 0 has retired the store that last read `buf`
           uint8_t* dst = buf + lane * line_bytes;
@@ -582,6 +591,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float* vv = reinterpret_cast<float*>(&v);
                 for (int i = 0; i < 4 && col + i < valid; ++i) vv[i] = p.Yin[off + i] + vv[i];
               }
+            }
+            if (p.bias || p.relu) {
+              const int64_t colb = g * p.cog + ncol0 + c0 + col;
+              float* vv = reinterpret_cast<float*>(&v);
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (col + i < valid) vv[i] = epi_apply(vv[i], p.bias, colb + i, p.relu);
             }
             if (p.out_f16) {
               __half* y = reinterpret_cast<__half*>(p.Y) + off;

@@ -285,6 +285,16 @@ __device__ __forceinline__ void tmem_ld_wait() {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// ---------------------------------------------------------------- fused epilogue
+
+// v + bias[col], then max(v, 0) exactly as the reference's max(x, 0.0)
+// (std::max: (v < 0) ? 0 : v, so NaN and -0.0 pass through like the interpreter).
+__device__ __forceinline__ float epi_apply(float v, const float* bias, int64_t col, int relu) {
+  if (bias) v = v + __ldg(bias + col);
+  if (relu) v = (v < 0.0f) ? 0.0f : v;
+  return v;
+}
+
 // ---------------------------------------------------------------- descriptors
 
 // UMMA shared-memory matrix descriptor (sm_100: version field = 1).

@@ -322,6 +322,23 @@ int encode_y(tb::IgemmParams& p, void* Y, int64_t rows, int out_f16) {
   return TIR_B200_OK;
 }
 
+// Fused epilogue (bias + ReLU) resolved from the C-ABI's optional struct.
+struct Epi {
+  const float* bias = nullptr;
+  int relu = 0;
+  bool on() const { return bias != nullptr || relu != 0; }
+  void apply(tb::IgemmParams& p) const { p.bias = bias; p.relu = relu; }
+};
+
+Epi make_epi(const tir_b200_epilogue* e) {
+  Epi r;
+  if (e) {
+    r.bias = e->bias;
+    r.relu = e->relu ? 1 : 0;
+  }
+  return r;
+}
+
 // Store mode for row-linear outputs: TMA store when every 32-column chunk lies
 // inside one group (or there is a single group), reduce-add for in-place
 // accumulate; otherwise the generic per-row path.
@@ -329,6 +346,8 @@ int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64
                     int out_f16) {
   p.store_mode = 0;
   if (getenv("TIR_B200_NO_TMA_STORE")) return TIR_B200_OK;
+  // Reduce-add cannot apply bias/ReLU after the add: accumulate + epilogue stays generic.
+  if (accumulate && (p.bias || p.relu)) return TIR_B200_OK;
   if (bn < 32 || !(p.groups == 1 || p.cog % 32 == 0) || (accumulate && Yin != Y)) return TIR_B200_OK;
   if ((reinterpret_cast<uintptr_t>(Y) & 15) || (p.ldy * (out_f16 ? 2 : 4)) % 16) return TIR_B200_OK;
   int rc = encode_y(p, Y, rows, out_f16);
@@ -398,7 +417,7 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
 // reference distribution are exact in any order, so parity is unchanged.
 int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int sms) {
   if (const char* e = getenv("TIR_B200_KSPLIT")) return std::max(1, atoi(e));
-  if (out_f16 || out_tiles * 2 > sms) return 1;
+  if (out_f16 || p.bias || p.relu || out_tiles * 2 > sms) return 1;  // epilogue needs the full sum
   int nst_min = 1 << 30;
   for (int i = 0; i < p.num_sub; ++i) nst_min = std::min(nst_min, p.sub[i].num_stages);
   int ks = static_cast<int>(std::min<int64_t>(sms / out_tiles, 8));
@@ -427,7 +446,7 @@ int prepare_split_output(tb::IgemmParams& p, void* Y, const float* Yin, int64_t 
 // ------------------------------------------------------------------ GMM
 
 int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
-             int64_t N, int64_t K, int accumulate, int out_f16, cudaStream_t stream) {
+             int64_t N, int64_t K, int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   if (M < 0 || N < 0 || K < 0) return set_err(TIR_B200_ERR_VALUE, "gmm: negative extent");
   if (M == 0 || N == 0) return TIR_B200_OK;
   if (K == 0) {  // C = Cin (or 0): nothing to contract
@@ -473,6 +492,7 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   p.out_f16 = out_f16;
   p.Y = C;
   p.Yin = Cin;
+  epi.apply(p);
   p.ksplit = 1;
   rc = finalize_tiles(p, bn, ks_eff);
   if (rc) return rc;
@@ -574,7 +594,7 @@ int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
 // Stride-1 2-D convolution as halo tiles (see halo.cuh). Returns kNotEligible
 // for shapes outside its envelope.
 int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
-                   int accumulate, int out_f16, cudaStream_t stream) {
+                   int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   if (getenv("TIR_B200_NO_HALO")) return kNotEligible;
   if (g.transposed || g.in[0] != 1 || g.k[0] != 1 || g.p[0] != 0) return kNotEligible;
   if (g.s[1] != 1 || g.s[2] != 1 || g.d[1] != g.d[2]) return kNotEligible;
@@ -629,6 +649,8 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   p.out_f16 = out_f16;
   p.Y = Y;
   p.Yin = Yin;
+  p.bias = epi.bias;
+  p.relu = epi.relu;
   // N tile: whole group width up to 256 when that still fills the machine.
   const int64_t spatial_tiles = g.n * p.tiles_h * p.tiles_w;
   const int bn = choose_bn(cog, spatial_tiles, g.g, taps * (cig / 16), di.sms);
@@ -666,10 +688,10 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   // updated in place (reduce-add). Otherwise direct register stores.
   p.store_mode = 0;
   p.stage_bytes = 0;
-  if (getenv("TIR_B200_STORE256") && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
+  if (getenv("TIR_B200_STORE256") && !epi.on() && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
       g.co % 8 == 0 && (reinterpret_cast<uintptr_t>(Y) & 31) == 0) {
     p.store_mode = 3;
-  } else if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || Yin == Y) &&
+  } else if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || (Yin == Y && !epi.on())) &&
       !getenv("TIR_B200_NO_TMA_STORE")) {
     const Driver* drv = driver();
     const int esz = out_f16 ? 2 : 4;
@@ -701,7 +723,7 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
 }
 
 int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,
-                 int accumulate, int out_f16, cudaStream_t stream) {
+                 int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   Geo g = g0;
   const uint16_t* X = X0;
   const uint16_t* W = W0;
@@ -742,10 +764,11 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     taps = g.k[0] * g.k[1];
   }
   // Channel padding (a bit-exact layout step): TMA needs a 16-byte pixel pitch.
+  // Channels are group-major, so padding each group's CI/G block is the same
+  // kernel over pixels x groups rows; weights pad their CI/G rows per tap.
   if (cig % 8) {
-    if (g.g != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "conv: grouped conv needs CI/G %% 8 == 0");
     const int64_t cip = (cig + 7) / 8 * 8;
-    const int64_t pix = g.n * g.in[0] * g.in[1] * g.in[2];
+    const int64_t pix = g.n * g.in[0] * g.in[1] * g.in[2] * g.g;
     const size_t xbytes = static_cast<size_t>(pix * cip * 2);
     const size_t wbytes = static_cast<size_t>(taps * cip * g.co * 2);
     void* ws = nullptr;
@@ -761,7 +784,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     ++g_launches;
     X = Xp;
     W = Wp;
-    g.ci = cip;
+    g.ci = cip * g.g;
     cig = cip;
   }
   const int box = pick_box(cig);
@@ -795,6 +818,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   p.out_f16 = out_f16;
   p.Y = Y;
   p.Yin = Yin;
+  epi.apply(p);
 
   const int lim_off = offset_limit(rank);
   if (!g.transposed) {
@@ -938,7 +962,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
 
 template <int K, int S>
 int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
-                    int accumulate, int out_f16, cudaStream_t stream) {
+                    int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   // 128 threads = 4 channel vectors x (TC/T) columns x (TR/R) rows
   constexpr int R = S == 1 ? 4 : 2, T = 2, TR = 8, TC = S == 1 ? 32 : 16;
   constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;
@@ -969,11 +993,15 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   p.tiles_w = static_cast<int32_t>((g.out[2] + TC - 1) / TC);
   p.cblocks = static_cast<int32_t>(g.ci / 32);
   p.accumulate = accumulate;
+  p.bias = epi.bias;
+  p.relu = epi.relu;
   p.out_f16 = out_f16;
   const int64_t blocks = g.n * p.tiles_h * p.tiles_w * p.cblocks;
   if (blocks >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many tiles");
   const size_t smem = 2 * static_cast<size_t>(FR) * FC * 32 * 2;  // two-slot ring
-  auto kern = tb::dep_tile_kernel<K, S, R, T, TR, TC>;
+  // The epilogue is a template flag so the plain kernel keeps its register budget.
+  auto kern = epi.on() ? tb::dep_tile_kernel<K, S, R, T, TR, TC, true>
+                       : tb::dep_tile_kernel<K, S, R, T, TR, TC, false>;
   CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
@@ -985,7 +1013,7 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
 }
 
 int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
-             int accumulate, int out_f16, cudaStream_t stream) {
+             int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   if (g.in[0] != 1 || g.k[0] != 1)
     return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: 2-D (NHWC) depthwise only");
   // Fast path: 3x3, stride 1 or 2, no dilation, 32-channel blocks, aligned operands.
@@ -994,8 +1022,8 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
                        (reinterpret_cast<uintptr_t>(X) % 16 == 0);
   if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 32 == 0 && g.k[1] == 3 && g.k[2] == 3 &&
       g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
-    return g.s[1] == 1 ? launch_dep_tile<3, 1>(g, X, W, Yin, Y, accumulate, out_f16, stream)
-                       : launch_dep_tile<3, 2>(g, X, W, Yin, Y, accumulate, out_f16, stream);
+    return g.s[1] == 1 ? launch_dep_tile<3, 1>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream)
+                       : launch_dep_tile<3, 2>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   }
   tb::DepParams p;
   p.X = reinterpret_cast<const __half*>(X);
@@ -1017,6 +1045,8 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
   p.dh = static_cast<int32_t>(g.d[1]);
   p.dw = static_cast<int32_t>(g.d[2]);
   p.accumulate = accumulate;
+  p.bias = epi.bias;
+  p.relu = epi.relu;
   p.out_f16 = out_f16;
   const DeviceInfo di = device_info();
   constexpr int R = 4;
@@ -1037,7 +1067,7 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
 }
 
 int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
-              const float* Yin, void* Y, int accumulate, int out_f16, cudaStream_t stream) {
+              const float* Yin, void* Y, int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
@@ -1045,11 +1075,11 @@ int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t*
   // Depthwise (CI/G == 1) is not a dense contraction: CUDA-core kernel.
   if (desc->op == TIR_B200_DEP || is_depthwise(g)) {
     if (!is_depthwise(g)) return set_err(TIR_B200_ERR_VALUE, "DEP requires groups == ci == co");
-    return dep_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+    return dep_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   }
-  rc = conv_halo_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+  rc = conv_halo_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   if (rc != kNotEligible) return rc;
-  return conv_tc_impl(g, X, W, Yin, Y, accumulate, out_f16, stream);
+  return conv_tc_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
 }
 
 // ------------------------------------------------------------------ host-buffer paths
@@ -1116,12 +1146,26 @@ int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]) 
 
 int tir_b200_gmm(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
                  int64_t N, int64_t K, int accumulate, int out_f16, void* stream) {
-  return gmm_impl(A, B, Cin, C, M, N, K, accumulate, out_f16, static_cast<cudaStream_t>(stream));
+  return gmm_impl(A, B, Cin, C, M, N, K, accumulate, out_f16, Epi{}, static_cast<cudaStream_t>(stream));
+}
+
+int tir_b200_gmm_ex(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, int64_t M,
+                    int64_t N, int64_t K, int accumulate, int out_f16, const tir_b200_epilogue* epi,
+                    void* stream) {
+  return gmm_impl(A, B, Cin, C, M, N, K, accumulate, out_f16, make_epi(epi),
+                  static_cast<cudaStream_t>(stream));
 }
 
 int tir_b200_conv(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
                   const float* Yin, void* Y, int accumulate, int out_f16, void* stream) {
-  return conv_impl(desc, X, W, Yin, Y, accumulate, out_f16, static_cast<cudaStream_t>(stream));
+  return conv_impl(desc, X, W, Yin, Y, accumulate, out_f16, Epi{}, static_cast<cudaStream_t>(stream));
+}
+
+int tir_b200_conv_ex(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
+                     const float* Yin, void* Y, int accumulate, int out_f16,
+                     const tir_b200_epilogue* epi, void* stream) {
+  return conv_impl(desc, X, W, Yin, Y, accumulate, out_f16, make_epi(epi),
+                   static_cast<cudaStream_t>(stream));
 }
 
 int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M, int64_t N,
@@ -1136,7 +1180,7 @@ int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M,
   CUDA_TRY(cudaMemcpyAsync(d + a, B, K * N * 2, cudaMemcpyHostToDevice, st));
   if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + a + b, C, M * N * 4, cudaMemcpyHostToDevice, st));
   rc = gmm_impl(reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + a),
-                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, st);
+                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, Epi{}, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(C, d + a + b, M * N * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1160,7 +1204,7 @@ int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const 
   CUDA_TRY(cudaMemcpyAsync(d + xa, W, we * 2, cudaMemcpyHostToDevice, st));
   if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + xa + wa, Y, ye * 4, cudaMemcpyHostToDevice, st));
   rc = conv_impl(desc, reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + xa),
-                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, st);
+                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, Epi{}, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1194,7 +1238,7 @@ int tir_b200_gmm_host_f32(const float* A, const float* B, float* C, int64_t M, i
   if (rc) return rc;
   if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + a + b, C, M * N * 4, cudaMemcpyHostToDevice, st));
   rc = gmm_impl(reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + a),
-                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, st);
+                reinterpret_cast<float*>(d + a + b), d + a + b, M, N, K, accumulate, 0, Epi{}, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(C, d + a + b, M * N * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
@@ -1225,7 +1269,7 @@ int tir_b200_conv_host_f32(const tir_b200_conv_desc* desc, const float* X, const
   if (rc) return rc;
   if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + xa + wa, Y, ye * 4, cudaMemcpyHostToDevice, st));
   rc = conv_impl(desc, reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + xa),
-                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, st);
+                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, Epi{}, st);
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));

@@ -94,6 +94,33 @@ def main():
         arrays[f"{key}/a"], arrays[f"{key}/b"], arrays[f"{key}/out"] = x, w, out
         meta[key] = {"kind": "conv", "spec": spec.__dict__, "dist": "D2"}
 
+    # 4. fused epilogues: the reference's own gemm_relu
+    # program (f32 params; random_tensor values are fp16-exact), then bias/relu
+    # stages appended to our programs by ir_gen.with_epilogue.
+    src = lib.tirref_workload_source(b"gemm_relu", 16, 0, 0, 0, 0, 0).decode()
+    ins = [ref_tensor(lib, (16, 16), 1), ref_tensor(lib, (16, 16), 2)]
+    out, _ = O.ref_run(src, ins, (16, 16))
+    arrays["ref_gemm_relu16/a"], arrays["ref_gemm_relu16/b"], arrays["ref_gemm_relu16/out"] = *ins, out
+    meta["ref_gemm_relu16"] = {"kind": "reference_workload", "source": ["gemm_relu", 16, 0, 0, 0, 0, 0],
+                               "seeds": [1, 2], "epilogue": {"bias": False, "relu": True}}
+    for name, base, bias, relu in [("GMM_24x40x56_bias_relu", "GMM_24x40x56", True, True),
+                                   ("C2D_bias_relu", "C2D", True, True), ("GRP_bias", "GRP", True, False),
+                                   ("T2D_relu", "T2D", False, True), ("DEP_bias_relu", "DEP", True, True)]:
+        a, b = arrays[f"{base}/a"], arrays[f"{base}/b"]
+        if base.startswith("GMM"):
+            m, n, k = GMM_CASES[base]
+            body, out_shape, m_ = G.gmm_source(m, n, k), (m, n), {"kind": "gmm", "mnk": [m, n, k]}
+        else:
+            spec = CASES[base]
+            body, out_shape, m_ = G.conv_source(spec), spec.y_shape(), {"kind": "conv", "spec": spec.__dict__}
+        ins = [a, b]
+        if bias:
+            ins.append(ref_tensor(lib, (out_shape[-1],), 5))
+            arrays[f"{name}/bias"] = ins[-1]
+        out, _ = O.ref_run(G.with_epilogue(body, out_shape, bias, relu), ins, out_shape)
+        arrays[f"{name}/a"], arrays[f"{name}/b"], arrays[f"{name}/out"] = a, b, out
+        meta[name] = {**m_, "dist": "D1", "epilogue": {"bias": bias, "relu": relu}}
+
     np.savez_compressed(os.path.join(HERE, "golden.npz"), **arrays)
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(meta, f, indent=1, default=list)

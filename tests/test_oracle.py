@@ -44,7 +44,7 @@ def test_restatement_matches_reference_golden(golden):
             got = O.conv(_spec(m), a, b)
         else:  # the reference's own workload programs
             which = m["source"][0]
-            if which == "matmul":
+            if which in ("matmul", "gemm_relu"):
                 got = O.gmm(a, b)
             elif which == "conv2d":
                 spec = G.ConvSpec("C2D", n=1, in_dhw=(1, 8, 8), ci=4, co=8, k=(1, 3, 3))
@@ -52,8 +52,33 @@ def test_restatement_matches_reference_golden(golden):
             else:
                 spec = G.ConvSpec("DEP", n=1, in_dhw=(1, 8, 8), ci=8, co=8, k=(1, 3, 3), groups=8)
                 got = O.conv(spec, a, b)
+        if "epilogue" in m:
+            got = O.epilogue(got, arrays.get(f"{name}/bias") if m["epilogue"]["bias"] else None,
+                             m["epilogue"]["relu"])
         assert got.shape == want.shape, name
         assert O.tensors_bitwise_equal(got, want), name
+
+
+def test_golden_epilogue_cases_present(golden):
+    meta, _ = golden
+    epi = {k for k, m in meta.items() if "epilogue" in m}
+    assert "ref_gemm_relu16" in epi  # the reference's own gemm_relu_source program
+    assert len(epi) >= 5
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="reference interpreter not built")
+@pytest.mark.parametrize("bias,relu", [(True, False), (False, True), (True, True)])
+def test_epilogue_oracle_matches_reference_interpreter(bias, relu):
+    """ir_gen.with_epilogue programs through tir::run vs oracle conv + epilogue,
+    on D2 (fp16 normals) where bias + relu see both signs and exact zeros."""
+    spec = G.ConvSpec("C2D", n=1, in_dhw=(1, 5, 6), ci=8, co=16, k=(1, 3, 3), p=(0, 1, 1))
+    x, w = O.normal_f16(spec.x_shape(), 31), O.normal_f16(spec.w_shape(), 32)
+    bvec = O.normal_f16((spec.co,), 33)
+    ins = [x, w] + ([bvec] if bias else [])
+    src = G.with_epilogue(G.conv_source(spec), spec.y_shape(), bias, relu)
+    want, _ = O.ref_run(src, ins, spec.y_shape())
+    got = O.epilogue(O.conv(spec, x, w), bvec if bias else None, relu)
+    assert O.tensors_bitwise_equal(got, want)
 
 
 def test_random_tensor_port_matches_reference_inputs(golden):

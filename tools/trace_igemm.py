@@ -58,6 +58,9 @@ def show(name, fn):
         print("tile %2d  epi_start %7d  epi_done %7d" % (i, a - t0, b - t0))
 
 
+At = torch.randn(128, 64, device=dev).half()
+Bt = torch.randn(64, 64, device=dev).half()
+show("GMM 128x64x64 (tiny)", lambda: tb.gmm(At, Bt))
 A = torch.randn(1024, 1024, device=dev).half()
 B = torch.randn(1024, 1024, device=dev).half()
 show("GMM 1024", lambda: tb.gmm(A, B))
