@@ -12,7 +12,10 @@
 #include <cstring>
 #include <vector>
 
+#include "tir/structural.h"
 #include "tir/text.h"
+#include "tir/validate.h"
+#include "tir_b200_tensorize.h"
 
 namespace tir_b200 {
 namespace {
@@ -153,15 +156,56 @@ std::string conv_intrin_name(const tir_b200_conv_desc& d) {
 }  // namespace tir_b200
 
 // ---------------------------------------------------------------------------
-// C entry point for the drop-in tests (tests/test_dropin.py, ctypes): parse a
-// program in the reference grammar, register the B200 intrinsic(s) on a fresh
-// ExecContext and run the reference interpreter, which dispatches every
-// tensorized block to the GPU through the HostKernels above.
+// C entry points for the drop-in tests (tests/test_dropin.py, ctypes). Errors
+// come back as "Kind|message" in `err`.
+namespace {
+
+void run_program(const tir::PrimFunc& f, tir::ExecContext& ctx, int n_in, const float* const* inputs,
+                 float* out, int64_t out_elems, int64_t* intrinsic_calls) {
+  auto in_params = tir::input_params(f);
+  if (static_cast<int>(in_params.size()) != n_in) tir::throw_error("ValueError", "input count mismatch");
+  std::vector<tir::TensorValue> vals;
+  for (int i = 0; i < n_in; ++i) {
+    tir::TensorValue t = tir::TensorValue::zeros(in_params[i]->dtype, in_params[i]->shape);
+    std::memcpy(t.data.data(), inputs[i], t.data.size());
+    vals.push_back(std::move(t));
+  }
+  auto outs = tir::run(f, vals, ctx);
+  if (intrinsic_calls) *intrinsic_calls = ctx.counters.intrinsic_calls;
+  if (outs.empty() || outs[0].num_elements() != out_elems)
+    tir::throw_error("ValueError", "unexpected output shape");
+  std::memcpy(out, outs[0].data.data(), static_cast<size_t>(out_elems) * 4);
+}
+
+template <typename F>
+int guarded(char* err, int errlen, F&& f) {
+  try {
+    f();
+    return 0;
+  } catch (const tir::Error& e) {
+    std::snprintf(err, static_cast<size_t>(errlen), "%s|%s", e.kind().c_str(), e.message().c_str());
+  } catch (const std::exception& e) {
+    std::snprintf(err, static_cast<size_t>(errlen), "InternalError|%s", e.what());
+  }
+  return -1;
+}
+
+void copy_out(const std::string& s, char* dst, int64_t len, const char* what) {
+  if (!dst) return;
+  if (static_cast<int64_t>(s.size()) + 1 > len) tir::throw_error("ValueError", std::string(what) + " buffer too small");
+  std::memcpy(dst, s.c_str(), s.size() + 1);
+}
+
+}  // namespace
+
+// Parse a program, register the B200 intrinsic on a fresh ExecContext and run
+// the reference interpreter, which dispatches every tensorized block to the
+// GPU through the HostKernels above.
 extern "C" int tir_b200_adapter_run(const char* ir_text, const char* intrin,
                                     const tir_b200_conv_desc* desc, int n_in,
                                     const float* const* inputs, float* out, int64_t out_elems,
                                     int64_t* intrinsic_calls, char* err, int errlen) {
-  try {
+  return guarded(err, errlen, [&] {
     tir::PrimFuncPtr f = tir::parse_text(ir_text);
     tir::ExecContext ctx;
     if (desc) {
@@ -169,26 +213,50 @@ extern "C" int tir_b200_adapter_run(const char* ir_text, const char* intrin,
     } else {
       tir_b200::register_gmm(ctx, intrin);
     }
-    auto in_params = tir::input_params(*f);
-    if (static_cast<int>(in_params.size()) != n_in)
-      tir::throw_error("ValueError", "input count mismatch");
-    std::vector<tir::TensorValue> vals;
-    for (int i = 0; i < n_in; ++i) {
-      tir::TensorValue t = tir::TensorValue::zeros(in_params[i]->dtype, in_params[i]->shape);
-      std::memcpy(t.data.data(), inputs[i], t.data.size());
-      vals.push_back(std::move(t));
+    run_program(*f, ctx, n_in, inputs, out, out_elems, intrinsic_calls);
+  });
+}
+
+// The tensorize composite on `block` of a scalar program: returns the rewritten
+// program text, its trace (JSONL), the generated intrinsic name and the match
+// (desc->op == TIR_B200_GMM with mnk for GMM). Also checks that the result is
+// validate_all-clean and that replaying the trace on a fresh parse of the
+// source reproduces it structurally (ValidationFailed / ReplayMismatch).
+extern "C" int tir_b200_adapter_tensorize(const char* ir_text, const char* block, char* text, int64_t text_len,
+                                          char* trace, int64_t trace_len, char* intrin, int64_t intrin_len,
+                                          tir_b200_conv_desc* desc, int64_t* mnk, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    tir_b200::register_tensorize_step_handler();
+    tir::Schedule s(tir::parse_text(ir_text));
+    tir_b200::OpMatch m = tir_b200::tensorize_whole_op(s, block);
+    auto diags = tir::validate_all(*s.func());
+    if (tir::has_errors(diags)) tir::throw_error("ValidationFailed", tir::format_diagnostic(diags.front()));
+    tir::Schedule again = tir::replay(s.trace(), tir::parse_text(ir_text));
+    if (!tir::structural_equal(*again.func(), *s.func())) tir::throw_error("ReplayMismatch", "trace replay differs");
+    copy_out(tir::print_text(s.func()), text, text_len, "text");
+    copy_out(tir::trace_to_jsonl(s.trace()), trace, trace_len, "trace");
+    copy_out(m.intrin, intrin, intrin_len, "intrin");
+    if (desc) {
+      *desc = m.conv;
+      if (m.gmm) desc->op = TIR_B200_GMM;
     }
-    auto outs = tir::run(*f, vals, ctx);
-    if (intrinsic_calls) *intrinsic_calls = ctx.counters.intrinsic_calls;
-    if (outs.empty() || outs[0].num_elements() != out_elems)
-      tir::throw_error("ValueError", "unexpected output shape");
-    std::memcpy(out, outs[0].data.data(), static_cast<size_t>(out_elems) * 4);
-    return 0;
-  } catch (const tir::Error& e) {
-    std::snprintf(err, static_cast<size_t>(errlen), "%s|%s", e.kind().c_str(), e.message().c_str());
-    return -1;
-  } catch (const std::exception& e) {
-    std::snprintf(err, static_cast<size_t>(errlen), "InternalError|%s", e.what());
-    return -1;
-  }
+    if (mnk) {
+      mnk[0] = m.m;
+      mnk[1] = m.n;
+      mnk[2] = m.k;
+    }
+  });
+}
+
+// Tensorize each named block of a scalar program, register the matched B200
+// kernels and run it through tir::run (blocks not named stay scalar).
+extern "C" int tir_b200_adapter_run_auto(const char* ir_text, const char* const* blocks, int n_blocks, int n_in,
+                                         const float* const* inputs, float* out, int64_t out_elems,
+                                         int64_t* intrinsic_calls, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    tir::Schedule s(tir::parse_text(ir_text));
+    tir::ExecContext ctx;
+    for (int i = 0; i < n_blocks; ++i) tir_b200::register_matched(ctx, tir_b200::tensorize_whole_op(s, blocks[i]));
+    run_program(*s.func(), ctx, n_in, inputs, out, out_elems, intrinsic_calls);
+  });
 }

@@ -60,14 +60,15 @@ def build_adapter(force: bool = False) -> str | None:
     (oracle/_ref/libtirkit.so); skipped where /root/reference is absent."""
     ref_lib = os.path.join(ROOT, "oracle", "_ref", "libtirkit.so")
     out = os.path.join(LIB, "libtir_b200_adapter.so")
-    src = os.path.join(PKG, "adapter", "tir_b200_adapter.cc")
-    hdr = os.path.join(PKG, "adapter", "tir_b200_adapter.h")
-    if not (os.path.isdir(REF) and os.path.exists(ref_lib) and os.path.exists(src)):
+    adir = os.path.join(PKG, "adapter")
+    srcs = [os.path.join(adir, f) for f in ("tir_b200_adapter.cc", "tir_b200_tensorize.cc")]
+    hdrs = [os.path.join(adir, f) for f in ("tir_b200_adapter.h", "tir_b200_tensorize.h")]
+    if not (os.path.isdir(REF) and os.path.exists(ref_lib) and all(map(os.path.exists, srcs))):
         return out if os.path.exists(out) else None
-    if force or _stale(out, [src, hdr, os.path.join(LIB, "libtir_b200.so"), ref_lib]):
+    if force or _stale(out, srcs + hdrs + [os.path.join(LIB, "libtir_b200.so"), ref_lib]):
         _run(["g++", "-std=gnu++20", "-O2", "-fPIC", "-shared", "-Wall", "-Wextra",
               f"-I{REF}/include", f"-I{ROOT}/include", f"-I{ROOT}/oracle/_ref/vendor",
-              "-o", out, src,
+              "-o", out, *srcs,
               f"-L{LIB}", "-ltir_b200", f"-L{ROOT}/oracle/_ref", "-ltirkit",
               "-Wl,-rpath,$ORIGIN", "-Wl,-rpath,$ORIGIN/../../oracle/_ref"])
     return out
