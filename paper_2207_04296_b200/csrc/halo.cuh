@@ -52,6 +52,8 @@ struct alignas(64) HaloParams {
   int32_t relu;       // fused epilogue: max(v, 0)
   int32_t store_mode;         // 0: direct register stores, 1: TMA store, 2: TMA reduce-add (Y += )
   int32_t nacc;               // TMEM accumulator buffers (MMA runs nacc-1 tiles ahead)
+  int32_t linear;             // 1: tile = 128 consecutive virtual pixels of the OH x Wv image
+                              //    (tiles_h tiles per image, tiles_w = 1; direct-store epilogue)
   int32_t stage_bytes;        // TMA-store staging buffer bytes (one of two)
   void* Y;
   const float* Yin;
@@ -99,7 +101,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], p.store_mode ? 128 : 256);  // modes 1-3 use warps 0-3
+      mbar_init(&tempty[i], p.store_mode ? 128 : 256);  // modes 1-3 use warps 0-3, mode 0 all 8
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -143,7 +145,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         int n, th, tw, g, nt;
         decompose(tile, n, th, tw, g, nt);
-        const int y0 = th * p.R - p.pad_h, x0 = tw * p.Wt - p.pad_w;
+        // linear: the slab starts at the first output row the 128-pixel window touches
+        const int y0 = (p.linear ? (th * 128) / p.Wv : th * p.R) - p.pad_h;
+        const int x0 = tw * p.Wt - p.pad_w;
         for (int cb = 0; cb < p.cblocks; ++cb, ++it) {
           mbar_wait(&empty[slot], phase ^ 1);
           if (trace && it < 128) trace[2 * it] = clock64();
@@ -213,7 +217,15 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       if (nslot == static_cast<uint32_t>(S)) { nslot = 0; nphase ^= 1; }
       if (last_cb && ++nacc == static_cast<uint32_t>(Cfg::kNacc)) { nacc = 0; nacc_phase ^= 1; }
       if (trace && lane == 0 && i < 128) trace[256 + 2 * i] = clock64();
-      const uint64_t a_slab = a0 + slot * slab16;
+      uint32_t lin_off = 0;  // linear tiles: window start within the slab's first row (16-B units)
+      if (p.linear) {
+        const int tile = static_cast<int>(blockIdx.x) + (i / p.cblocks) * static_cast<int>(gridDim.x);
+        int n, th, tw, g, nt;
+        decompose(tile, n, th, tw, g, nt);
+        const int v0 = th * 128;
+        lin_off = static_cast<uint32_t>(v0 - (v0 / p.Wv) * p.Wv) * 8u;
+      }
+      const uint64_t a_slab = a0 + slot * slab16 + lin_off;
       const uint64_t b_cb = b0 + ((static_cast<uint32_t>(cb * 64) * Cfg::kBRowBytes) >> 4);
       auto issue_tap = [&](int ty, int tx, int t) {
         const uint64_t a = a_slab + static_cast<uint32_t>(ty * wv_dil + tx * dil8);
@@ -385,9 +397,18 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       int n, th, tw, g, nt;
       decompose(tile, n, th, tw, g, nt);
       auto row_offset = [&](int m) -> int64_t {
-        const int ry = m / p.Wv, cx = m - ry * p.Wv;
-        const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
-        if (ry >= p.R || cx >= p.Wt || oy >= p.oh || ox >= p.ow) return -1;
+        int oy, ox;
+        if (p.linear) {  // virtual pixel v of the OH x Wv image; columns >= OW are discarded
+          const int v = th * 128 + m;
+          oy = v / p.Wv;
+          ox = v - oy * p.Wv;
+        } else {
+          const int ry = m / p.Wv, cx = m - ry * p.Wv;
+          if (ry >= p.R || cx >= p.Wt) return -1;
+          oy = th * p.R + ry;
+          ox = tw * p.Wt + cx;
+        }
+        if (oy >= p.oh || ox >= p.ow) return -1;
         return ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + g * p.cog + nt * BN;
       };
       const int64_t off_lo = row_offset(r_lo), off_hi = row_offset(r_hi);

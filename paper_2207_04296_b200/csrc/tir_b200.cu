@@ -613,10 +613,33 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
     if (Wt < 16) return kNotEligible;
   }
   const int64_t Wv = Wt + (KW - 1) * d;
-  const int64_t HR = R + (KH - 1) * d;
-  if (Wv > 256 || HR > 256) return kNotEligible;
+  int64_t HR = R + (KH - 1) * d;
   const int64_t max_off = (KH - 1) * d * Wv + (KW - 1) * d;
+  const DeviceInfo di0 = device_info();
+  // Linear tiles (full-width rows only): a tile is 128 consecutive virtual pixels
+  // of the OH x Wv virtual output image instead of R whole rows. Waste drops from
+  // (128 - R*OW)/128 to (Wv - OW)/Wv and the tile count no longer rounds up per
+  // row block (C2D 56x56: 448 -> 416 tiles, i.e. 3 instead of 4 per SM). The slab
+  // covers every row a window starting anywhere in a row can touch.
+  // Opt-in (TIR_B200_HALO_LINEAR=1): measured on B200 the bigger slab and the
+  // direct-store epilogue add more SMEM/LSU traffic per tile than the saved wave
+  // costs (C2D paper shape 9.7 -> 10.9 us), because the kernel is SMEM-bound.
+  bool linear = false;
+  if (Wt == OW && getenv("TIR_B200_HALO_LINEAR")) {
+    const int64_t rect = g.n * ((OH + R - 1) / R);
+    const int64_t lin = g.n * ((OH * Wv + 127) / 128);
+    const int64_t lin_hr = (Wv - 1 + 127) / Wv + 1 + (KH - 1) * d;
+    const int64_t sms = di0.sms;
+    const int64_t lin_rows = std::max(lin_hr * Wv, Wv - 1 + max_off + 128);
+    if ((lin + sms - 1) / sms < (rect + sms - 1) / sms && lin_hr <= 256 && lin_rows <= tb::kHaloMaxRows) {
+      linear = true;
+      R = 1;
+      HR = lin_hr;
+    }
+  }
+  if (Wv > 256 || HR > 256) return kNotEligible;
   int64_t slab_rows = std::max(HR * Wv, max_off + 128);
+  if (linear) slab_rows = std::max(slab_rows, Wv - 1 + max_off + 128);
   slab_rows = (slab_rows + 7) / 8 * 8;
   if (slab_rows > tb::kHaloMaxRows) return kNotEligible;
   const int64_t taps = KH * KW;
@@ -641,7 +664,8 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   p.Wv = static_cast<int32_t>(Wv);
   p.HR = static_cast<int32_t>(HR);
   p.tiles_w = static_cast<int32_t>((OW + Wt - 1) / Wt);
-  p.tiles_h = static_cast<int32_t>((OH + R - 1) / R);
+  p.tiles_h = static_cast<int32_t>(linear ? (OH * Wv + 127) / 128 : (OH + R - 1) / R);
+  p.linear = linear ? 1 : 0;
   p.cblocks = static_cast<int32_t>(cig / 64);
   p.b_rows = static_cast<int32_t>(taps * cig);
   p.slab_rows = static_cast<int32_t>(slab_rows);
@@ -688,7 +712,9 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   // updated in place (reduce-add). Otherwise direct register stores.
   p.store_mode = 0;
   p.stage_bytes = 0;
-  if (getenv("TIR_B200_STORE256") && !epi.on() && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
+  if (linear) {
+    // direct register stores (generic mode 0): a linear tile is not a TMA box
+  } else if (getenv("TIR_B200_STORE256") && !epi.on() && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
       g.co % 8 == 0 && (reinterpret_cast<uintptr_t>(Y) & 31) == 0) {
     p.store_mode = 3;
   } else if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || (Yin == Y && !epi.on())) &&
