@@ -314,6 +314,60 @@ def traffic_from_profiles(name):
         return None
 
 
+# ----------------------------------------------------------------------------- networks
+
+NET_BATCH = {"resnet50": 32, "mobilenet_v2": 64}  # per GPU (weak scaling: global = N x this)
+
+
+def measure_nets(device, world, rank, dist, steps, names):
+    """Batch-sharded network forwards: every rank builds the graph of
+    its shard of the global batch (replicated weights, no collective), captures it
+    in a CUDA graph and replays it `steps` times between CUDA events; images/s =
+    global batch x steps / max-over-ranks time."""
+    import torch
+
+    from paper_2207_04296_b200 import nets
+
+    out = {}
+    for name in names:
+        per_gpu = NET_BATCH[name]
+        global_batch = per_gpu * world
+        net, (lo, hi) = nets.build_shard(name, global_batch, rank, world)
+        dn = nets.DeviceNet(net, device)
+        dn.input.normal_()
+        dn.capture()
+        for _ in range(3):
+            dn.replay()
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(dn.stream):  # graph replays go to the current stream
+            e0.record(dn.stream)
+            for _ in range(steps):
+                dn.graph.replay()
+            e1.record(dn.stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1)
+        if dist:
+            t = torch.tensor([ms], device=device)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms = float(t.item())
+        sec = ms / 1e3
+        out[name] = {
+            "images_per_s": round(global_batch * steps / sec, 1),
+            "tflops": round(net.flops * world * steps / sec / 1e12, 2),
+            "ms_per_forward": round(ms / steps, 4),
+            "batch_per_gpu": per_gpu, "global_batch": global_batch, "image": net.input_shape[1],
+            "launches_per_forward": nets.launches_per_forward(net),
+            "sharding": f"batch across {world} GPU(s), no collective" if world > 1 else "single GPU",
+            "dtype": "fp16 activations / fp32 accumulate",
+        }
+        del dn
+        torch.cuda.empty_cache()
+    return out
+
+
 # ----------------------------------------------------------------------------- CPU reference
 
 def cpu_reference_sample(name, budget_s, threads):
@@ -393,6 +447,8 @@ def main():
     ap.add_argument("--no-ops", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nets", action="store_true", help="skip the batch-sharded network forwards")
+    ap.add_argument("--nets", default="resnet50,mobilenet_v2")
     ap.add_argument("--profile", metavar="OP", help="eager launches of one op for ncu (no timing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -458,6 +514,14 @@ def main():
             except Exception as e:  # report, never hide
                 ops[other] = {"error": str(e)[:200]}
 
+    net_lines = {}
+    if not args.no_nets:
+        try:
+            net_lines = measure_nets(device, world, rank, dist, max(5, min(args.steps, 20)),
+                                     [n for n in args.nets.split(",") if n])
+        except Exception as e:  # report, never hide
+            net_lines = {"error": str(e)[:300]}
+
     e2e = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(name, args.steps)
@@ -498,6 +562,7 @@ def main():
             "clocks": clocks,
             "gpu_launches": launches,
             "ops": ops,
+            "nets": net_lines,
         }
         print(json.dumps(line), flush=True)
     if dist:

@@ -73,13 +73,23 @@ typedef struct {
 } tir_b200_conv_desc;
 
 /* Fused epilogue, applied per output element after the
- * reduction, in this order:  v = acc;  v = Yin + v (accumulate);  v = v + bias[col];
- * v = max(v, 0) (relu). `bias` is fp32 per output column (GMM: N, conv: CO);
- * either field may be 0/NULL. gemm + relu is the reference's gemm_relu_source
- * workload (tests/testing/workloads.h:61-91) as one intrinsic. */
+ * reduction, in this order:
+ *   v = acc;  v = Yin + v (accumulate);  v = v + bias[col];  v = v + residual[elem];
+ *   v = act(v).
+ * `bias` is fp32 per output column (GMM: N, conv: CO); `residual` is fp16 with
+ * Y's shape and layout (a ResNet / MobileNet shortcut); `relu` selects act:
+ *   0 none, 1 ReLU max(v, 0), 2 ReLU6 min(max(v, 0), 6), 3 GELU (erf form).
+ * Every field may be 0/NULL. gemm + relu is the reference's gemm_relu_source
+ * workload (tests/testing/workloads.h:61-91) as one intrinsic. DEP supports
+ * bias and act but not residual. */
+#define TIR_B200_ACT_NONE 0
+#define TIR_B200_ACT_RELU 1
+#define TIR_B200_ACT_RELU6 2
+#define TIR_B200_ACT_GELU 3
 typedef struct {
   const float* bias;
   int32_t relu;
+  const uint16_t* residual;
 } tir_b200_epilogue;
 
 /* Library / device facts. */
@@ -131,6 +141,23 @@ int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M,
 
 int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
                        float* Y, int accumulate);
+
+/* ---- network-graph glue, device pointers, asynchronous ----
+ * fp16 NHWC / row-major operands, 16-byte aligned, channel / column counts a
+ * multiple of 8. The networks' contractions (every conv / GEMM, with bias,
+ * residual and activation fused) go through tir_b200_conv_ex / tir_b200_gmm_ex. */
+/* Y[n, OH, OW, c] = max over k x k windows (stride s, padding p never wins). */
+int tir_b200_maxpool2d(const uint16_t* X, uint16_t* Y, int64_t n, int64_t h, int64_t w, int64_t c,
+                       int64_t k, int64_t s, int64_t p, void* stream);
+/* Y[n, c] = fp16(sum over hw pixels of X[n, hw, c] / hw), fp32 sum. */
+int tir_b200_avgpool_global(const uint16_t* X, uint16_t* Y, int64_t n, int64_t hw, int64_t c,
+                            void* stream);
+/* Y[r, :] = LayerNorm(X[r, :]) * gamma + beta (fp32 statistics), cols <= 8192. */
+int tir_b200_layernorm(const uint16_t* X, uint16_t* Y, const float* gamma, const float* beta,
+                       int64_t rows, int64_t cols, float eps, void* stream);
+/* Y[r, :] = softmax(scale * X[r, :]) (fp32 internally), cols <= 8192. */
+int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols, float scale,
+                     void* stream);
 
 /* Frees the calling thread's cached device/pinned buffers. */
 void tir_b200_release_host_cache(void);

@@ -8,6 +8,10 @@ from .api import (  # noqa: F401
     Conv,
     TirError,
     compulsory_bytes,
+    avgpool_global,
+    layernorm,
+    maxpool2d,
+    softmax,
     conv,
     conv_host,
     gmm,

@@ -98,8 +98,13 @@ class Conv:
 
 
 class Epilogue(ctypes.Structure):
-    """tir_b200_epilogue: optional per-column fp32 bias, then ReLU (include/tir_b200.h)."""
-    _fields_ = [("bias", ctypes.c_void_p), ("relu", ctypes.c_int32)]
+    """tir_b200_epilogue: optional per-column fp32 bias, fp16 residual, then an
+    activation (include/tir_b200.h)."""
+    _fields_ = [("bias", ctypes.c_void_p), ("relu", ctypes.c_int32), ("residual", ctypes.c_void_p)]
+
+
+ACT_NONE, ACT_RELU, ACT_RELU6, ACT_GELU = 0, 1, 2, 3
+_ACTS = {None: 0, False: 0, True: 1, "none": 0, "relu": 1, "relu6": 2, "gelu": 3, 0: 0, 1: 1, 2: 2, 3: 3}
 
 
 _lib = None
@@ -124,6 +129,10 @@ def lib() -> ctypes.CDLL:
         L.tir_b200_gmm_host.argtypes = [vp, vp, vp, i64, i64, i64, i32]
         L.tir_b200_conv_host.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, i32]
         L.tir_b200_gmm_host_f32.argtypes = [vp, vp, vp, i64, i64, i64, i32]
+        L.tir_b200_maxpool2d.argtypes = [vp, vp, i64, i64, i64, i64, i64, i64, i64, vp]
+        L.tir_b200_avgpool_global.argtypes = [vp, vp, i64, i64, i64, vp]
+        L.tir_b200_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, ctypes.c_float, vp]
+        L.tir_b200_softmax.argtypes = [vp, vp, i64, i64, ctypes.c_float, vp]
         L.tir_b200_conv_host_f32.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, i32]
         _lib = L
     return _lib
@@ -170,23 +179,32 @@ def _need(t, dtype, shape, name):
     del torch
 
 
-def _epilogue(bias, relu, cols, device):
-    """Builds the C-ABI epilogue; None when neither bias nor relu is requested."""
-    if bias is None and not relu:
+def _epilogue(bias, relu, cols, device, residual=None, out_shape=None):
+    """Builds the C-ABI epilogue; None when nothing is requested. `relu` is a bool
+    (ReLU) or an activation name/code: "relu", "relu6", "gelu"."""
+    if relu not in _ACTS:
+        raise TirError("ValueError", f"unknown activation {relu!r}")
+    act = _ACTS[relu]
+    if bias is None and not act and residual is None:
         return None
     torch = _torch()
     if bias is not None:
         _need(bias, torch.float32, (cols,), "bias")
         if bias.device != device:
             raise TirError("ValueError", "bias must live on the operands' device")
-    return Epilogue(bias.data_ptr() if bias is not None else None, int(bool(relu)))
+    if residual is not None:
+        _need(residual, torch.float16, out_shape, "residual")
+        if residual.device != device:
+            raise TirError("ValueError", "residual must live on the operands' device")
+    return Epilogue(bias.data_ptr() if bias is not None else None, act,
+                    residual.data_ptr() if residual is not None else None)
 
 
 def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, bias=None,
-        relu: bool = False, stream=None):
+        relu=False, residual=None, stream=None):
     """C (+)= A @ B with A [M,K] fp16, B [K,N] fp16 (N contiguous), fp32 accumulation.
-    Optional fused epilogue: C = relu((C +) A @ B + bias[N]).
-    Returns C ([M,N] fp32, or fp16 if out_f16)."""
+    Optional fused epilogue: C = act((C +) A @ B + bias[N] + residual[M,N]), act from
+    `relu` (True / "relu", "relu6", "gelu"). Returns C ([M,N] fp32, or fp16 if out_f16)."""
     torch = _torch()
     M, K = A.shape
     N = B.shape[1]
@@ -199,7 +217,7 @@ def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, bias=N
     _need(C, torch.float16 if out_f16 else torch.float32, (M, N), "C")
     if accumulate and out_f16:
         raise TirError("ValueError", "accumulate requires an fp32 C")
-    epi = _epilogue(bias, relu, N, A.device)
+    epi = _epilogue(bias, relu, N, A.device, residual, (M, N))
     if epi is None:
         _check(lib().tir_b200_gmm(_ptr(A), _ptr(B), _ptr(C) if accumulate else None, _ptr(C), M, N, K,
                                   int(accumulate), int(out_f16), _stream(stream)))
@@ -211,9 +229,10 @@ def gmm(A, B, C=None, *, accumulate: bool = False, out_f16: bool = False, bias=N
 
 
 def conv(spec: Conv, X, W, Y=None, *, accumulate: bool = False, out_f16: bool = False,
-         bias=None, relu: bool = False, stream=None):
+         bias=None, relu=False, residual=None, stream=None):
     """Y (+)= conv(X, W) for C1D/C2D/C3D/DIL/GRP/T2D/DEP (layouts: include/tir_b200.h).
-    Optional fused epilogue: Y = relu((Y +) conv(X, W) + bias[CO])."""
+    Optional fused epilogue: Y = act((Y +) conv(X, W) + bias[CO] + residual), residual
+    fp16 with Y's shape (not for DEP); act from `relu` (True / "relu", "relu6", "gelu")."""
     torch = _torch()
     _need(X, torch.float16, spec.x_shape(), "X")
     _need(W, torch.float16, spec.w_shape(), "W")
@@ -226,7 +245,7 @@ def conv(spec: Conv, X, W, Y=None, *, accumulate: bool = False, out_f16: bool = 
     if accumulate and out_f16:
         raise TirError("ValueError", "accumulate requires an fp32 Y")
     d = spec.desc()
-    epi = _epilogue(bias, relu, spec.co, X.device)
+    epi = _epilogue(bias, relu, spec.co, X.device, residual, spec.y_shape())
     if epi is None:
         _check(lib().tir_b200_conv(ctypes.byref(d), _ptr(X), _ptr(W), _ptr(Y) if accumulate else None,
                                    _ptr(Y), int(accumulate), int(out_f16), _stream(stream)))
@@ -234,6 +253,60 @@ def conv(spec: Conv, X, W, Y=None, *, accumulate: bool = False, out_f16: bool = 
         _check(lib().tir_b200_conv_ex(ctypes.byref(d), _ptr(X), _ptr(W),
                                       _ptr(Y) if accumulate else None, _ptr(Y), int(accumulate),
                                       int(out_f16), ctypes.byref(epi), _stream(stream)))
+    return Y
+
+
+# ---------------------------------------------------------------- network glue
+
+def maxpool2d(X, k: int, s: int, p: int, Y=None, *, stream=None):
+    """NHWC fp16 max pooling (padding never wins); returns Y [N, OH, OW, C]."""
+    torch = _torch()
+    n, h, w, c = X.shape
+    _need(X, torch.float16, (n, h, w, c), "X")
+    oh, ow = (h + 2 * p - k) // s + 1, (w + 2 * p - k) // s + 1
+    if Y is None:
+        Y = torch.empty((n, oh, ow, c), dtype=torch.float16, device=X.device)
+    _need(Y, torch.float16, (n, oh, ow, c), "Y")
+    _check(lib().tir_b200_maxpool2d(_ptr(X), _ptr(Y), n, h, w, c, k, s, p, _stream(stream)))
+    return Y
+
+
+def avgpool_global(X, Y=None, *, stream=None):
+    """NHWC fp16 [N, H, W, C] -> [N, C] fp16 mean over pixels (fp32 sum)."""
+    torch = _torch()
+    n, h, w, c = X.shape
+    _need(X, torch.float16, (n, h, w, c), "X")
+    if Y is None:
+        Y = torch.empty((n, c), dtype=torch.float16, device=X.device)
+    _need(Y, torch.float16, (n, c), "Y")
+    _check(lib().tir_b200_avgpool_global(_ptr(X), _ptr(Y), n, h * w, c, _stream(stream)))
+    return Y
+
+
+def layernorm(X, gamma, beta, eps: float = 1e-12, Y=None, *, stream=None):
+    """Row LayerNorm of fp16 X [rows, cols] with fp32 gamma/beta; fp16 out."""
+    torch = _torch()
+    rows, cols = X.shape
+    _need(X, torch.float16, (rows, cols), "X")
+    _need(gamma, torch.float32, (cols,), "gamma")
+    _need(beta, torch.float32, (cols,), "beta")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _need(Y, torch.float16, (rows, cols), "Y")
+    _check(lib().tir_b200_layernorm(_ptr(X), _ptr(Y), _ptr(gamma), _ptr(beta), rows, cols, eps,
+                                    _stream(stream)))
+    return Y
+
+
+def softmax(X, scale: float = 1.0, Y=None, *, stream=None):
+    """Row softmax(scale * X) of fp16 X [rows, cols]; fp16 out."""
+    torch = _torch()
+    rows, cols = X.shape
+    _need(X, torch.float16, (rows, cols), "X")
+    if Y is None:
+        Y = torch.empty_like(X)
+    _need(Y, torch.float16, (rows, cols), "Y")
+    _check(lib().tir_b200_softmax(_ptr(X), _ptr(Y), rows, cols, scale, _stream(stream)))
     return Y
 
 

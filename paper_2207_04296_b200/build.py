@@ -29,7 +29,7 @@ NVCC_FLAGS = [
 ]
 
 SOURCES = ["csrc/tir_b200.cu"]
-HEADERS = ["csrc/ptx.cuh", "csrc/igemm.cuh", "csrc/halo.cuh", "csrc/dep.cuh", "csrc/prep.cuh",
+HEADERS = ["csrc/ptx.cuh", "csrc/igemm.cuh", "csrc/halo.cuh", "csrc/dep.cuh", "csrc/prep.cuh", "csrc/netops.cuh",
            "../include/tir_b200.h"]
 
 

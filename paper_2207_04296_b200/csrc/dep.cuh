@@ -116,10 +116,7 @@ __global__ void __launch_bounds__(256) dep_kernel(const DepParams p) {
       const int oy = oy0 + r;
       if (oy >= p.oh) break;
       const int64_t off = ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0;
-      if (p.bias || p.relu) {
-#pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[r][v] = epi_apply(acc[r][v], p.bias, c0 + v, p.relu);
-      }
+      if (p.bias || p.relu) epi_run<VEC>(acc[r], p.bias, c0, VEC, nullptr, p.relu);
       if (p.out_f16) {
         __half* y = reinterpret_cast<__half*>(p.Y) + off;
         if constexpr (VEC == 8) {
@@ -203,6 +200,9 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
   constexpr int CT = 32;
   static_assert(TR == (128 / (4 * (TC / T))) * R, "128 threads = 4 channel vectors x TC/T cols x TR/R rows");
   constexpr uint32_t kTileBytes = FR * FC * CT * 2;
+  // ring slots start on 128-byte boundaries (TMA destination alignment; the
+  // stride-2 footprint 17 x 33 x 64 B is not a multiple of 128)
+  constexpr uint32_t kSlotBytes = (kTileBytes + 127) / 128 * 128;
   // Persistent: the block walks tiles b, b + grid, ... with a two-slot TMA ring,
   // so the next tile's input streams in while this one is computed and stored.
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
     int n, oy0, ox0, c0;
     tile_coords(t, n, oy0, ox0, c0);
     mbar_arrive_expect_tx(&bar[slot], kTileBytes);
-    tma_load_4d(smem_raw + slot * kTileBytes, &p.tmX, &bar[slot], c0, ox0 * S - p.pad_w,
+    tma_load_4d(smem_raw + slot * kSlotBytes, &p.tmX, &bar[slot], c0, ox0 * S - p.pad_w,
                 oy0 * S - p.pad_h, n);
   };
 
@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
       }
     if (slot == 0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; }
     else { mbar_wait(&bar[1], phase1); phase1 ^= 1; }
-    const __half* tile = reinterpret_cast<const __half*>(smem_raw + slot * kTileBytes);
+    const __half* tile = reinterpret_cast<const __half*>(smem_raw + slot * kSlotBytes);
     const __half* my = tile + ((tr * R * S) * FC + tc * T * S) * CT + cv * 8;
 #pragma unroll
     for (int iy = 0; iy < fr; ++iy) {
@@ -324,13 +324,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
         float2 f[4];
 #pragma unroll
         for (int v = 0; v < 4; ++v) f[v] = unpack_f32x2(acc[r][tt][v]);
-        if (EPI) {
-#pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            f[v].x = epi_apply(f[v].x, p.bias, c0 + cv * 8 + 2 * v, p.relu);
-            f[v].y = epi_apply(f[v].y, p.bias, c0 + cv * 8 + 2 * v + 1, p.relu);
-          }
-        }
+        if (EPI) epi_run<8>(reinterpret_cast<float*>(f), p.bias, c0 + cv * 8, 8, nullptr, p.relu);
         if (p.out_f16) {
           uint4 u;
           __half2 hh[4];

@@ -49,7 +49,8 @@ struct alignas(64) HaloParams {
   int32_t slab_rows;          // smem rows per slab (>= max tap offset + 128)
   int32_t accumulate, out_f16;
   const float* bias;  // fused epilogue: per-output-column bias (nullable)
-  int32_t relu;       // fused epilogue: max(v, 0)
+  int32_t relu;       // fused epilogue activation (1 ReLU, 2 ReLU6, 3 GELU)
+  const uint16_t* residual;  // fused epilogue: fp16 residual in Y's layout (store_mode 0 only)
   int32_t store_mode;         // 0: direct register stores, 1: TMA store, 2: TMA reduce-add (Y += )
   int32_t nacc;               // TMEM accumulator buffers (MMA runs nacc-1 tiles ahead)
   int32_t linear;             // 1: tile = 128 consecutive virtual pixels of the OH x Wv image
@@ -327,12 +328,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
           tmem_ld_wait();
-          if (p.bias || p.relu) {
+          if (p.bias || p.relu || p.residual) {
             const int64_t colb = g * p.cog + nt * BN + c0;
             const int lim = p.cog - (nt * BN + c0);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < lim) r[i] = __float_as_uint(epi_apply(__uint_as_float(r[i]), p.bias, colb + i, p.relu));
+            const uint16_t* res = nullptr;
+            if (p.residual && mine) {
+              const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
+              if (oy < p.oh && ox < p.ow)
+                res = p.residual + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + colb;
+            }
+            epi_run<32>(reinterpret_cast<float*>(r), p.bias, colb, lim, res, p.relu);
           }
           uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
           named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store
@@ -446,10 +451,12 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
                 v0 = p.Yin[off] + v0;
               }
             }
-            if (p.bias || p.relu) {
+            if (p.bias || p.relu || p.residual) {
               const int64_t colb = g * p.cog + ncol0 + c0 + col;
-              v0 = epi_apply(v0, p.bias, colb, p.relu);
-              if (pair) v1 = epi_apply(v1, p.bias, colb + 1, p.relu);
+              float vv[2] = {v0, v1};
+              epi_run<2>(vv, p.bias, colb, pair ? 2 : 1, p.residual ? p.residual + off : nullptr, p.relu);
+              v0 = vv[0];
+              v1 = vv[1];
             }
             if (p.out_f16) {
               __half* y = reinterpret_cast<__half*>(p.Y) + off;

@@ -92,7 +92,8 @@ struct alignas(64) IgemmParams {
   int32_t out_dims[3]; // OW, OH, OD
   int32_t accumulate;
   const float* bias;  // fused epilogue: per-output-column bias (nullable)
-  int32_t relu;       // fused epilogue: max(v, 0)
+  int32_t relu;       // fused epilogue activation (1 ReLU, 2 ReLU6, 3 GELU)
+  const uint16_t* residual;  // fused epilogue: fp16 residual in Y's layout
   int32_t out_f16;
   int32_t stages;      // smem ring depth
   int32_t b_res_rows;  // B_RESIDENT: rows of the resident panel (multiple of 64)
@@ -448,11 +449,13 @@ __global__ void __launch_bounds__(kThreads, 1)
       // one bulk tensor store (or reduce-add for accumulate) per chunk; two
       // staging buffers per warp. Row-linear outputs only (GMM, forward conv).
       const int line_bytes = p.out_f16 ? 64 : 128;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      int local = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
         int s, mt, g, nt;
         decompose_tile(p, tile, s, mt, g, nt);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
         constexpr int kCols = BN < 32 ? BN : 32;
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += kCols, ++chunk) {
@@ -460,12 +463,13 @@ __global__ void __launch_bounds__(kThreads, 1)
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
           tmem_ld_wait();
           if (nt * BN + c0 >= p.cog) continue;  // warp-uniform: chunk past the group
-          if (p.bias || p.relu) {
+          if (p.bias || p.relu || p.residual) {
             const int64_t colb = g * p.cog + nt * BN + c0;
             const int lim = p.cog - (nt * BN + c0);
-#pragma unroll
-            for (int i = 0; i < 32; ++i)
-              if (i < lim) r[i] = __float_as_uint(epi_apply(__uint_as_float(r[i]), p.bias, colb + i, p.relu));
+            const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
+            // rows past M are clipped by the TMA store; their residual is never read
+            const uint16_t* res = (p.residual && row < p.sub[0].m_count) ? p.residual + row * p.ldy + colb : nullptr;
+            epi_run<32>(reinterpret_cast<float*>(r), p.bias, colb, lim, res, p.relu);
           }
           uint8_t* buf = wbuf + (chunk & 1) * 4096;
           __syncwarp();  // lane 0 has retired the store that last read `buf`
@@ -501,6 +505,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             tma_store_wait_read<1>();
           }
         }
+        if (trace && threadIdx.x == 0 && local < 64) trace[513 + 2 * local] = clock64();
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
@@ -518,7 +523,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) &&
                           ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
                           (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      int local = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
         int s, mt, g, nt;
         decompose_tile(p, tile, s, mt, g, nt);
         const SubProb& sp = p.sub[s];
@@ -542,6 +548,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
         const int ncol0 = nt * BN;
         constexpr int kChunk = BN < 32 ? BN : 32;
         constexpr int kLanesPerRow = kChunk / 4;
@@ -592,12 +599,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int i = 0; i < 4 && col + i < valid; ++i) vv[i] = p.Yin[off + i] + vv[i];
               }
             }
-            if (p.bias || p.relu) {
+            if (p.bias || p.relu || p.residual) {
               const int64_t colb = g * p.cog + ncol0 + c0 + col;
-              float* vv = reinterpret_cast<float*>(&v);
-#pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (col + i < valid) vv[i] = epi_apply(vv[i], p.bias, colb + i, p.relu);
+              epi_run<4>(reinterpret_cast<float*>(&v), p.bias, colb, valid - col,
+                         p.residual ? p.residual + off : nullptr, p.relu);
             }
             if (p.out_f16) {
               __half* y = reinterpret_cast<__half*>(p.Y) + off;
@@ -623,6 +628,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
           __syncwarp();
         }
+        if (trace && threadIdx.x == 0 && local < 64) trace[513 + 2 * local] = clock64();
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
         if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {

@@ -289,10 +289,91 @@ __device__ __forceinline__ void tmem_ld_wait() {
 
 // v + bias[col], then max(v, 0) exactly as the reference's max(x, 0.0)
 // (std::max: (v < 0) ? 0 : v, so NaN and -0.0 pass through like the interpreter).
-__device__ __forceinline__ float epi_apply(float v, const float* bias, int64_t col, int relu) {
-  if (bias) v = v + __ldg(bias + col);
-  if (relu) v = (v < 0.0f) ? 0.0f : v;
+// act: 1 ReLU, 2 ReLU6, 3 GELU (erf form, BERT); 0 none. ReLU is the reference's
+// max(x, 0.0) (std::max: (v < 0) ? 0 : v, so NaN and -0.0 pass through).
+__device__ __forceinline__ float epi_act(float v, int act) {
+  if (act == 1) return (v < 0.0f) ? 0.0f : v;
+  if (act == 2) return (v < 0.0f) ? 0.0f : (v > 6.0f ? 6.0f : v);
+  if (act == 3) return 0.5f * v * (1.0f + erff(v * 0.70710678118654752f));
   return v;
+}
+
+// erf-form GELU on four values, out of line: inlined into every unrolled
+// epilogue loop the erff polynomial would bloat the kernels' hot loops.
+__device__ __noinline__ float4 gelu4(float4 t) {
+  const float k = 0.70710678118654752f;
+  t.x = 0.5f * t.x * (1.0f + erff(t.x * k));
+  t.y = 0.5f * t.y * (1.0f + erff(t.y * k));
+  t.z = 0.5f * t.z * (1.0f + erff(t.z * k));
+  t.w = 0.5f * t.w * (1.0f + erff(t.w * k));
+  return t;
+}
+
+// In-place activation of N values; the branch on `act` is warp-uniform and sits
+// outside the element loop so the loop body is straight-line code.
+template <int N>
+__device__ __forceinline__ void epi_act_n(float* v, int act) {
+  if (act == 1) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = (v[i] < 0.0f) ? 0.0f : v[i];
+  } else if (act == 2) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) v[i] = (v[i] < 0.0f) ? 0.0f : (v[i] > 6.0f ? 6.0f : v[i]);
+  } else if (act == 3) {
+#pragma unroll
+    for (int i = 0; i + 4 <= N; i += 4) {
+      const float4 t = gelu4(make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+      v[i] = t.x; v[i + 1] = t.y; v[i + 2] = t.z; v[i + 3] = t.w;
+    }
+#pragma unroll
+    for (int i = N / 4 * 4; i < N; ++i) v[i] = 0.5f * v[i] * (1.0f + erff(v[i] * 0.70710678118654752f));
+  }
+}
+
+// Fused epilogue on N consecutive columns [col, col + N) of one output row, in
+// the C-ABI order: v + bias[col + i], + residual[i], act. `lim` columns are
+// valid (the rest lie past a group / tensor edge: never loaded, never stored by
+// the caller). Bias and residual are fetched with 16-byte loads when the whole
+// run is valid and aligned, so an epilogue chunk issues a handful of independent
+// loads instead of N dependent ones.
+template <int N>
+__device__ __forceinline__ void epi_run(float* v, const float* bias, int64_t col, int lim,
+                                        const uint16_t* res, int act) {
+  if (bias) {
+    const float* b = bias + col;
+    if (N % 4 == 0 && lim >= N && (reinterpret_cast<uintptr_t>(b) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i += 4) {
+        const float4 t = __ldg(reinterpret_cast<const float4*>(b + i));
+        v[i] += t.x; v[i + 1] += t.y; v[i + 2] += t.z; v[i + 3] += t.w;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        if (i < lim) v[i] += __ldg(b + i);
+    }
+  }
+  if (res) {
+    if (N % 8 == 0 && lim >= N && (reinterpret_cast<uintptr_t>(res) & 15) == 0) {
+#pragma unroll
+      for (int i = 0; i < N; i += 8) {
+        const uint4 u = __ldg(reinterpret_cast<const uint4*>(res + i));
+        const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = __half22float2(h[j]);
+          v[i + 2 * j] += f.x;
+          v[i + 2 * j + 1] += f.y;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i)
+        if (i < lim)
+          v[i] += __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short*>(res) + i)));
+    }
+  }
+  epi_act_n<N>(v, act);
 }
 
 // ---------------------------------------------------------------- descriptors

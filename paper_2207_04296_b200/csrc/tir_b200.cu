@@ -22,6 +22,7 @@
 #include "dep.cuh"
 #include "halo.cuh"
 #include "igemm.cuh"
+#include "netops.cuh"
 #include "prep.cuh"
 
 namespace {
@@ -326,15 +327,17 @@ int encode_y(tb::IgemmParams& p, void* Y, int64_t rows, int out_f16) {
 struct Epi {
   const float* bias = nullptr;
   int relu = 0;
-  bool on() const { return bias != nullptr || relu != 0; }
-  void apply(tb::IgemmParams& p) const { p.bias = bias; p.relu = relu; }
+  const uint16_t* residual = nullptr;
+  bool on() const { return bias != nullptr || relu != 0 || residual != nullptr; }
+  void apply(tb::IgemmParams& p) const { p.bias = bias; p.relu = relu; p.residual = residual; }
 };
 
 Epi make_epi(const tir_b200_epilogue* e) {
   Epi r;
   if (e) {
     r.bias = e->bias;
-    r.relu = e->relu ? 1 : 0;
+    r.relu = e->relu;
+    r.residual = e->residual;
   }
   return r;
 }
@@ -417,7 +420,7 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
 // reference distribution are exact in any order, so parity is unchanged.
 int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int sms) {
   if (const char* e = getenv("TIR_B200_KSPLIT")) return std::max(1, atoi(e));
-  if (out_f16 || p.bias || p.relu || out_tiles * 2 > sms) return 1;  // epilogue needs the full sum
+  if (out_f16 || p.bias || p.relu || p.residual || out_tiles * 2 > sms) return 1;  // epilogue needs the full sum
   int nst_min = 1 << 30;
   for (int i = 0; i < p.num_sub; ++i) nst_min = std::min(nst_min, p.sub[i].num_stages);
   int ks = static_cast<int>(std::min<int64_t>(sms / out_tiles, 8));
@@ -675,6 +678,7 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   p.Yin = Yin;
   p.bias = epi.bias;
   p.relu = epi.relu;
+  p.residual = epi.residual;
   // N tile: whole group width up to 256 when that still fills the machine.
   const int64_t spatial_tiles = g.n * p.tiles_h * p.tiles_w;
   const int bn = choose_bn(cog, spatial_tiles, g.g, taps * (cig / 16), di.sms);
@@ -1024,7 +1028,7 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   p.out_f16 = out_f16;
   const int64_t blocks = g.n * p.tiles_h * p.tiles_w * p.cblocks;
   if (blocks >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many tiles");
-  const size_t smem = 2 * static_cast<size_t>(FR) * FC * 32 * 2;  // two-slot ring
+  const size_t smem = 2 * ((static_cast<size_t>(FR) * FC * 32 * 2 + 127) / 128 * 128);  // two-slot ring
   // The epilogue is a template flag so the plain kernel keeps its register budget.
   auto kern = epi.on() ? tb::dep_tile_kernel<K, S, R, T, TR, TC, true>
                        : tb::dep_tile_kernel<K, S, R, T, TR, TC, false>;
@@ -1042,6 +1046,7 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
              int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   if (g.in[0] != 1 || g.k[0] != 1)
     return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: 2-D (NHWC) depthwise only");
+  if (epi.residual) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: residual epilogue not supported");
   // Fast path: 3x3, stride 1 or 2, no dilation, 32-channel blocks, aligned operands.
   const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0) &&
                        (!accumulate || reinterpret_cast<uintptr_t>(Yin) % 16 == 0) &&
@@ -1299,6 +1304,86 @@ int tir_b200_conv_host_f32(const tir_b200_conv_desc* desc, const float* X, const
   if (rc) return rc;
   CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
+  return TIR_B200_OK;
+}
+
+// ---- network-graph glue
+
+static int check_vec(const void* a, const void* b, int64_t c) {
+  if (!a || !b) return set_err(TIR_B200_ERR_VALUE, "null operand");
+  if ((reinterpret_cast<uintptr_t>(a) & 15) || (reinterpret_cast<uintptr_t>(b) & 15))
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "operands must be 16-byte aligned");
+  if (c <= 0 || c % 8) return set_err(TIR_B200_ERR_UNSUPPORTED, "channels/cols must be a positive multiple of 8");
+  return TIR_B200_OK;
+}
+
+int tir_b200_maxpool2d(const uint16_t* X, uint16_t* Y, int64_t n, int64_t h, int64_t w, int64_t c,
+                       int64_t k, int64_t s, int64_t p, void* stream) {
+  int rc = check_vec(X, Y, c);
+  if (rc) return rc;
+  if (n < 0 || h <= 0 || w <= 0 || k <= 0 || s <= 0 || p < 0 || p >= k)
+    return set_err(TIR_B200_ERR_VALUE, "maxpool2d: bad geometry");
+  const int64_t oh = (h + 2 * p - k) / s + 1, ow = (w + 2 * p - k) / s + 1;
+  if (oh <= 0 || ow <= 0) return set_err(TIR_B200_ERR_VALUE, "maxpool2d: empty output");
+  const int64_t total = n * oh * ow * (c / 8);
+  if (total == 0) return TIR_B200_OK;
+  const DeviceInfo di = device_info();
+  const int grid = static_cast<int>(std::min<int64_t>((total + 255) / 256, di.sms * 16));
+  tb::maxpool2d_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      X, Y, (int)n, (int)h, (int)w, (int)c, (int)oh, (int)ow, (int)k, (int)s, (int)p);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int tir_b200_avgpool_global(const uint16_t* X, uint16_t* Y, int64_t n, int64_t hw, int64_t c, void* stream) {
+  int rc = check_vec(X, Y, c);
+  if (rc) return rc;
+  if (n < 0 || hw <= 0 || n > 65535) return set_err(TIR_B200_ERR_VALUE, "avgpool_global: bad geometry");
+  if (n == 0) return TIR_B200_OK;
+  const int cv = static_cast<int>(c / 8);
+  dim3 grid((cv + 63) / 64, static_cast<unsigned>(n));
+  tb::avgpool_global_kernel<<<grid, 64, 0, static_cast<cudaStream_t>(stream)>>>(X, Y, (int)hw, (int)c);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int tir_b200_layernorm(const uint16_t* X, uint16_t* Y, const float* gamma, const float* beta, int64_t rows,
+                       int64_t cols, float eps, void* stream) {
+  int rc = check_vec(X, Y, cols);
+  if (rc) return rc;
+  if (!gamma || !beta) return set_err(TIR_B200_ERR_VALUE, "layernorm: null gamma/beta");
+  if (cols > 8192 || rows < 0 || rows >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "layernorm: shape");
+  if (rows == 0) return TIR_B200_OK;
+  const int cv = static_cast<int>(cols / 8);
+  const int threads = std::min(256, (cv + 31) / 32 * 32);
+  const int vpt = (cv + threads - 1) / threads;
+  auto st = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>(rows);
+  if (vpt == 1) tb::layernorm_kernel<1><<<g, threads, 0, st>>>(X, Y, gamma, beta, (int)cols, eps);
+  else if (vpt == 2) tb::layernorm_kernel<2><<<g, threads, 0, st>>>(X, Y, gamma, beta, (int)cols, eps);
+  else tb::layernorm_kernel<4><<<g, threads, 0, st>>>(X, Y, gamma, beta, (int)cols, eps);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols, float scale, void* stream) {
+  int rc = check_vec(X, Y, cols);
+  if (rc) return rc;
+  if (cols > 8192 || rows < 0 || rows >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "softmax: shape");
+  if (rows == 0) return TIR_B200_OK;
+  const int cv = static_cast<int>(cols / 8);
+  const int threads = std::min(256, (cv + 31) / 32 * 32);
+  const int vpt = (cv + threads - 1) / threads;
+  auto st = static_cast<cudaStream_t>(stream);
+  const unsigned g = static_cast<unsigned>(rows);
+  if (vpt == 1) tb::softmax_kernel<1><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
+  else if (vpt == 2) tb::softmax_kernel<2><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
+  else tb::softmax_kernel<4><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
   return TIR_B200_OK;
 }
 

@@ -1,0 +1,135 @@
+"""GPU tests of the network graphs: ResNet-50 and
+MobileNet-V2 forwards through the C-ABI (every conv / GEMM on the tcgen05
+kernels with fused bias / residual / ReLU(6), DEP on the CUDA-core kernel, the
+pooling glue) against the float64 CPU replay of the same op list
+(oracle/nets_ref.py), which rounds activations to fp16 exactly where the device
+graph does. Tolerance: the device reassociates fp32 sums inside the tensor
+cores, which flips an fp16 rounding now and then; those 1-ulp (2^-11) flips
+propagate but stay far below 2% of the logit range.
+
+Also: the glue kernels alone (exact: max is exact, mean / LayerNorm / softmax
+to fp32 rounding), the fused residual epilogue on both conv paths, CUDA-graph
+replay == eager, and batch-shard consistency (two half-batch graphs == one
+full-batch graph)."""
+import numpy as np
+import pytest
+import torch
+
+import paper_2207_04296_b200 as tb
+from paper_2207_04296_b200 import nets
+
+pytestmark = pytest.mark.gpu
+
+LOGIT_TOL = 2e-2
+
+
+def _rel(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-6))
+
+
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2"])
+def test_network_matches_cpu_reference(name, cuda):
+    from oracle import nets_ref
+
+    net = nets.NETS[name](2, image=64)
+    dn = nets.DeviceNet(net, cuda)
+    x = np.random.default_rng(1).standard_normal(net.input_shape).astype(np.float16)
+    dn.input.copy_(torch.from_numpy(x))
+    with torch.cuda.stream(dn.stream):
+        dn.run()
+    dn.stream.synchronize()
+    got = dn.output.reshape(2, -1).cpu().numpy()
+    want = nets_ref.forward(net, x)
+    assert np.isfinite(got).all()
+    assert _rel(got, want) < LOGIT_TOL, _rel(got, want)
+    assert (got.argmax(1) == want.argmax(1)).all()
+
+
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2"])
+def test_graph_replay_equals_eager_and_shards(name, cuda):
+    net = nets.NETS[name](4, image=64)
+    dn = nets.DeviceNet(net, cuda)
+    x = torch.randn(net.input_shape, device=cuda).half()
+    dn.input.copy_(x)
+    with torch.cuda.stream(dn.stream):
+        dn.run()
+    dn.stream.synchronize()
+    eager = dn.output.clone()
+    dn.capture()
+    dn.output.zero_()
+    dn.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(dn.output, eager)
+    # two ranks' shards (same seed = replicated weights), evaluated independently
+    parts = []
+    for r in range(2):
+        sub, (lo, hi) = nets.build_shard(name, 4, r, 2, image=64)
+        ds = nets.DeviceNet(sub, cuda)
+        ds.input.copy_(x[lo:hi])
+        with torch.cuda.stream(ds.stream):
+            ds.run()
+        ds.stream.synchronize()
+        parts.append(ds.output)
+    full = torch.cat(parts)
+    assert _rel(full.cpu().numpy(), eager.cpu().numpy()) < 1e-2
+
+
+def test_maxpool_avgpool_exact(cuda):
+    g = torch.Generator(device=cuda).manual_seed(3)
+    x = torch.randn(3, 17, 15, 24, device=cuda, generator=g).half()
+    y = tb.maxpool2d(x, 3, 2, 1)
+    want = torch.nn.functional.max_pool2d(x.float().permute(0, 3, 1, 2), 3, 2, 1).permute(0, 2, 3, 1)
+    assert torch.equal(y.float(), want)
+    a = tb.avgpool_global(x)
+    wa = x.double().mean(dim=(1, 2)).half()
+    assert (a.float() - wa.float()).abs().max().item() <= 1e-3 * wa.float().abs().max().item()
+
+
+def test_layernorm_softmax(cuda):
+    g = torch.Generator(device=cuda).manual_seed(4)
+    x = torch.randn(37, 1024, device=cuda, generator=g).half()
+    gamma = torch.randn(1024, device=cuda, generator=g)
+    beta = torch.randn(1024, device=cuda, generator=g)
+    y = tb.layernorm(x, gamma, beta, 1e-12)
+    want = torch.nn.functional.layer_norm(x.double(), (1024,), gamma.double(), beta.double(), 1e-12)
+    assert (y.double() - want).abs().max().item() < 2e-2
+    s = tb.softmax(x, 0.125)
+    ws = torch.softmax(x.double() * 0.125, dim=-1)
+    assert (s.double() - ws).abs().max().item() < 1e-3
+
+
+@pytest.mark.parametrize("shape", [
+    dict(op="C2D", n=2, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), p=(0, 1, 1)),        # halo path
+    dict(op="C2D", n=2, in_dhw=(1, 15, 15), ci=64, co=128, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1)),  # im2col
+])
+@pytest.mark.parametrize("act", ["relu", "relu6", "none"])
+def test_conv_residual_epilogue(shape, act, cuda):
+    from oracle import oracle as O
+
+    spec = tb.Conv(**shape)
+    X = O.reference_tensor(spec.x_shape(), 1)
+    W = O.reference_tensor(spec.w_shape(), 2)
+    R = O.reference_tensor(spec.y_shape(), 3)
+    bias = O.reference_tensor((spec.co,), 4)
+    got = tb.conv(spec, torch.from_numpy(X).to(cuda).half(), torch.from_numpy(W).to(cuda).half(),
+                  bias=torch.from_numpy(bias).to(cuda), relu=act,
+                  residual=torch.from_numpy(R).to(cuda).half()).cpu().numpy()
+    v = O.conv(O.ConvSpec(**shape), X, W, threads=8) + bias + R  # exact on the reference distribution
+    if act == "relu":
+        v = np.maximum(v, 0)
+    elif act == "relu6":
+        v = np.clip(v, 0, 6)
+    assert O.tensors_bitwise_equal(got, v.astype(np.float32))
+
+
+def test_gmm_residual_gelu(cuda):
+    g = torch.Generator(device=cuda).manual_seed(5)
+    a = torch.randn(256, 128, device=cuda, generator=g).half()
+    b = torch.randn(128, 96, device=cuda, generator=g).half()
+    r = torch.randn(256, 96, device=cuda, generator=g).half()
+    bias = torch.randn(96, device=cuda, generator=g)
+    y = tb.gmm(a, b, out_f16=True, bias=bias, residual=r, relu="gelu")
+    want = torch.nn.functional.gelu(a.double() @ b.double() + bias.double() + r.double())
+    assert (y.double() - want).abs().max().item() < 2e-2
+    with pytest.raises(tb.TirError):
+        tb.gmm(a, b, relu="swish")

@@ -64,6 +64,9 @@ SMALL = {
     "T2D_k3": tb.Conv("T2D", n=1, in_dhw=(1, 5, 6), ci=64, co=32, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), transposed=True),
     "DEP": tb.Conv("DEP", n=2, in_dhw=(1, 9, 9), ci=32, co=32, k=(1, 3, 3), p=(0, 1, 1), groups=32),
     "DEP_s2": tb.Conv("DEP", n=2, in_dhw=(1, 28, 28), ci=96, co=96, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), groups=96),
+    # more tiles than resident blocks: exercises the second TMA ring slot (128-B aligned)
+    "DEP_s2_ring": tb.Conv("DEP", n=8, in_dhw=(1, 112, 112), ci=96, co=96, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
+                           groups=96),
     "DEP_c12": tb.Conv("DEP", n=1, in_dhw=(1, 7, 7), ci=12, co=12, k=(1, 5, 5), p=(0, 2, 2), groups=12),
 }
 
