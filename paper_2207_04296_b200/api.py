@@ -20,7 +20,8 @@ from dataclasses import dataclass, replace
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "lib", "libtir_b200.so")
+# TIR_B200_LIB overrides the library path (A/B timing of two builds of the same ABI)
+LIB_PATH = os.environ.get("TIR_B200_LIB") or os.path.join(PKG, "lib", "libtir_b200.so")
 
 OK, ERR_VALUE, ERR_UNSUPPORTED, ERR_CUDA = 0, 1, 2, 3
 _KINDS = {ERR_VALUE: "ValueError", ERR_UNSUPPORTED: "UnsupportedShape", ERR_CUDA: "CudaError"}

@@ -317,9 +317,31 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       const int line = ry * p.Wt + cx;
       const int line_bytes = p.out_f16 ? 64 : 128;
       uint32_t acc = 0, acc_phase = 0, chunk = 0;
+      // Bias fetched before the accumulator wait (one column per lane, then
+      // shuffled), the residual of the next 32 columns in flight during the
+      // current chunk: loads issued next to their use stall the chunk chain.
+      const bool epi_on = p.bias || p.relu || p.residual;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         int n, th, tw, g, nt;
         decompose(tile, n, th, tw, g, nt);
+        const int64_t col_tile = static_cast<int64_t>(g) * p.cog + nt * BN;
+        const int valid_tile = p.cog - nt * BN;
+        // bias of the next 32 columns, one column per lane (prefetched a chunk ahead)
+        float bnext = (p.bias && static_cast<int>(lane) < valid_tile) ? __ldg(p.bias + col_tile + lane) : 0.0f;
+        const uint16_t* res_row = nullptr;
+        if (p.residual && mine) {
+          const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
+          if (oy < p.oh && ox < p.ow)
+            res_row = p.residual + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + col_tile;
+        }
+        uint4 rp[4];
+        auto fetch_res = [&](int c) {
+          if (res_row && valid_tile - c >= 32 && (reinterpret_cast<uintptr_t>(res_row + c) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rp[i] = __ldg(reinterpret_cast<const uint4*>(res_row + c) + i);
+          }
+        };
+        fetch_res(0);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (trace && threadIdx.x == 0) trace[512 + 2 * (tile / gridDim.x)] = clock64();
@@ -328,16 +350,38 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
           tmem_ld_wait();
-          if (p.bias || p.relu || p.residual) {
-            const int64_t colb = g * p.cog + nt * BN + c0;
-            const int lim = p.cog - (nt * BN + c0);
-            const uint16_t* res = nullptr;
-            if (p.residual && mine) {
-              const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
-              if (oy < p.oh && ox < p.ow)
-                res = p.residual + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + colb;
+          if (epi_on) {
+            float* v = reinterpret_cast<float*>(r);
+            const int lim = valid_tile - c0;
+            if (p.bias) {
+              const float bcur = bnext;
+              const int nc = c0 + 32 + static_cast<int>(lane);
+              bnext = nc < valid_tile ? __ldg(p.bias + col_tile + nc) : 0.0f;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bcur, i);
             }
-            epi_run<32>(reinterpret_cast<float*>(r), p.bias, colb, lim, res, p.relu);
+            if (res_row) {
+              if (lim >= 32 && (reinterpret_cast<uintptr_t>(res_row + c0) & 15) == 0) {
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const __half2* hv = reinterpret_cast<const __half2*>(&rp[i]);
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    const float2 f = __half22float2(hv[j]);
+                    v[8 * i + 2 * j] += f.x;
+                    v[8 * i + 2 * j + 1] += f.y;
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                  if (i < lim)
+                    v[i] += __half2float(__ushort_as_half(
+                        __ldg(reinterpret_cast<const unsigned short*>(res_row + c0) + i)));
+              }
+              fetch_res(c0 + 32);
+            }
+            epi_act_n<32>(v, p.relu);
           }
           uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
           named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store

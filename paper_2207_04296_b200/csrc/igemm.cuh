@@ -101,6 +101,7 @@ struct alignas(64) IgemmParams {
   void* Y;
   const float* Yin;
   int32_t store_mode;  // 0: generic row-offset stores, 1: TMA store, 2: TMA reduce-add (Y += tile)
+  int32_t epi_cw;      // store modes 1/2: columns per staged chunk (32, or 64 for fp16 with BN >= 64)
   int32_t ksplit;      // split-K partitions (>= 1); > 1 adds partials into a pre-initialised Y
   int32_t reduce;      // generic path: red.global.add into Y instead of stores (split-K)
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
@@ -445,62 +446,122 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t acc = 0, acc_phase = 0, chunk = 0;
     if (p.store_mode) {
       // TMA store: thread = tile row (tcgen05.ld 32x32b); each warp stages its
-      // 32 rows x 32 columns (SW128 / SW64 swizzled, conflict-free) and issues
+      // 32 rows x cw columns (SW128 / SW64 swizzled, conflict-free) and issues
       // one bulk tensor store (or reduce-add for accumulate) per chunk; two
-      // staging buffers per warp. Row-linear outputs only (GMM, forward conv).
-      const int line_bytes = p.out_f16 ? 64 : 128;
+      // staging buffers per warp. fp16 outputs with BN >= 64 stage 64 columns
+      // (two 32-column TMEM loads) as 128-byte rows: the store engine is
+      // request-bound, and 4 KB requests double the bytes per request of the
+      // 2 KB ones (1x1 convs / expansion GEMMs are epilogue-bound).
+      // Row-linear outputs only (GMM, forward conv).
+      // Epilogue operands are fetched ahead of their use (measured: a bias load
+      // issued next to its add costs ~1000 cycles per 32 columns under the
+      // store traffic): the tile's bias is loaded before the accumulator wait,
+      // one column per lane (then broadcast with shuffles), and the residual of
+      // the next 32 columns is in flight while the current ones are processed.
+      const int cw = p.epi_cw;  // 32, or 64 for fp16 output
+      const int line_bytes = cw * (p.out_f16 ? 2 : 4);
+      const bool epi_on = p.bias || p.relu || p.residual;
       int local = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
         int s, mt, g, nt;
         decompose_tile(p, tile, s, mt, g, nt);
+        const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
+        const int64_t col_tile = static_cast<int64_t>(g) * p.cog + nt * BN;
+        const int valid_tile = p.cog - nt * BN;  // columns of this tile inside the group
+        // bias of the next 32 columns, one column per lane (prefetched a chunk ahead)
+        float bnext = (p.bias && static_cast<int>(lane) < valid_tile) ? __ldg(p.bias + col_tile + lane) : 0.0f;
+        // residual rows past M are clipped by the TMA store and never read
+        const uint16_t* res_row = (p.residual && row < p.sub[0].m_count) ? p.residual + row * p.ldy + col_tile
+                                                                         : nullptr;
+        uint4 rp[4];  // fp16 residual of the next 32 columns
+        auto fetch_res = [&](int c) {
+          if (res_row && valid_tile - c >= 32 && (reinterpret_cast<uintptr_t>(res_row + c) & 15) == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; ++i) rp[i] = __ldg(reinterpret_cast<const uint4*>(res_row + c) + i);
+          }
+        };
+        fetch_res(0);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
-        constexpr int kCols = BN < 32 ? BN : 32;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += kCols, ++chunk) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
-          tmem_ld_wait();
-          if (nt * BN + c0 >= p.cog) continue;  // warp-uniform: chunk past the group
-          if (p.bias || p.relu || p.residual) {
-            const int64_t colb = g * p.cog + nt * BN + c0;
-            const int lim = p.cog - (nt * BN + c0);
-            const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
-            // rows past M are clipped by the TMA store; their residual is never read
-            const uint16_t* res = (p.residual && row < p.sub[0].m_count) ? p.residual + row * p.ldy + colb : nullptr;
-            epi_run<32>(reinterpret_cast<float*>(r), p.bias, colb, lim, res, p.relu);
-          }
+        for (int c0 = 0; c0 < BN; c0 += cw, ++chunk) {
+          if (c0 >= valid_tile) continue;  // warp-uniform: chunk past the group
           uint8_t* buf = wbuf + (chunk & 1) * 4096;
-          __syncwarp();  // lane 0 has retired the store that last read `buf`
           uint8_t* dst = buf + lane * line_bytes;
-          if (p.out_f16) {
+          __syncwarp();  // lane 0 has retired the store that last read `buf`
+#pragma unroll 1
+          for (int h = 0; h < cw; h += 32) {
+            uint32_t r[32];
+            const int cc = c0 + h;
+            tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + cc, r);
+            tmem_ld_wait();
+            const int lim = valid_tile - cc;
+            if (lim <= 0) break;  // warp-uniform: half past the group (TMA clips it)
+            if (epi_on) {
+              float* v = reinterpret_cast<float*>(r);
+              // C-ABI order: + bias, + residual, activation
+              if (p.bias) {
+                const float bcur = bnext;
+                const int nc = cc + 32 + static_cast<int>(lane);
+                bnext = nc < valid_tile ? __ldg(p.bias + col_tile + nc) : 0.0f;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 u;
-              __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * c]), __uint_as_float(r[8 * c + 1]));
-              __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * c + 2]), __uint_as_float(r[8 * c + 3]));
-              __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * c + 4]), __uint_as_float(r[8 * c + 5]));
-              __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * c + 6]), __uint_as_float(r[8 * c + 7]));
-              u.x = *reinterpret_cast<uint32_t*>(&h0);
-              u.y = *reinterpret_cast<uint32_t*>(&h1);
-              u.z = *reinterpret_cast<uint32_t*>(&h2);
-              u.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(dst + ((c ^ ((lane >> 1) & 3)) << 4)) = u;  // SW64
+                for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bcur, i);
+              }
+              if (res_row) {
+                if (lim >= 32 && (reinterpret_cast<uintptr_t>(res_row + cc) & 15) == 0) {
+#pragma unroll
+                  for (int i = 0; i < 4; ++i) {
+                    const __half2* hv = reinterpret_cast<const __half2*>(&rp[i]);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                      const float2 f = __half22float2(hv[j]);
+                      v[8 * i + 2 * j] += f.x;
+                      v[8 * i + 2 * j + 1] += f.y;
+                    }
+                  }
+                } else {
+#pragma unroll
+                  for (int i = 0; i < 32; ++i)
+                    if (i < lim)
+                      v[i] += __half2float(__ushort_as_half(
+                          __ldg(reinterpret_cast<const unsigned short*>(res_row + cc) + i)));
+                }
+                fetch_res(cc + 32);  // in flight during this chunk's conversion and store
+              }
+              epi_act_n<32>(v, p.relu);
             }
-          } else {
+            if (p.out_f16) {
+              const int hp = h >> 3;  // first 16-byte piece of this half (0 or 4)
 #pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<uint4*>(dst + ((c ^ (lane & 7)) << 4)) =
-                  make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);  // SW128
+              for (int c = 0; c < 4; ++c) {
+                uint4 u;
+                __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * c]), __uint_as_float(r[8 * c + 1]));
+                __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * c + 2]), __uint_as_float(r[8 * c + 3]));
+                __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * c + 4]), __uint_as_float(r[8 * c + 5]));
+                __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * c + 6]), __uint_as_float(r[8 * c + 7]));
+                u.x = *reinterpret_cast<uint32_t*>(&h0);
+                u.y = *reinterpret_cast<uint32_t*>(&h1);
+                u.z = *reinterpret_cast<uint32_t*>(&h2);
+                u.w = *reinterpret_cast<uint32_t*>(&h3);
+                const int piece = cw == 64 ? ((hp + c) ^ (lane & 7))          // SW128
+                                           : (c ^ ((lane >> 1) & 3));         // SW64
+                *reinterpret_cast<uint4*>(dst + (piece << 4)) = u;
+              }
+            } else {
+#pragma unroll
+              for (int c = 0; c < 8; ++c)
+                *reinterpret_cast<uint4*>(dst + ((c ^ (lane & 7)) << 4)) =
+                    make_uint4(r[4 * c], r[4 * c + 1], r[4 * c + 2], r[4 * c + 3]);  // SW128
+            }
           }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            const int col = g * p.cog + nt * BN + c0;
-            const int row = mt * kBM + static_cast<int>(q) * 32;
-            if (p.store_mode == 2) tma_reduce_add_2d(&p.tmY, buf, col, row);
-            else tma_store_2d(&p.tmY, buf, col, row);
+            const int col = static_cast<int>(col_tile) + c0;
+            const int row0 = mt * kBM + static_cast<int>(q) * 32;
+            if (p.store_mode == 2) tma_reduce_add_2d(&p.tmY, buf, col, row0);
+            else tma_store_2d(&p.tmY, buf, col, row0);
             tma_store_commit();
             tma_store_wait_read<1>();
           }

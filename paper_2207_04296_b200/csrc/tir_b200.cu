@@ -307,17 +307,22 @@ int choose_ks(int max_pieces, int box, int bn) {
 }
 
 // Y as a 2-D [rows, ldy] map for the per-warp TMA-store epilogue.
-int encode_y(tb::IgemmParams& p, void* Y, int64_t rows, int out_f16) {
+// Box {cw, 32}: one epilogue warp's 32 rows x a staged chunk of cw columns
+// (32; 64 for fp16 output when BN >= 64 and no chunk crosses a group, so every
+// staged row is 128 bytes), swizzled like the staging buffer.
+int encode_y(tb::IgemmParams& p, void* Y, int64_t rows, int out_f16, int bn) {
   const Driver* d = driver();
   if (!d->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
   const int esz = out_f16 ? 2 : 4;
+  p.epi_cw = (out_f16 && bn >= 64 && (p.groups == 1 || p.cog % 64 == 0)) ? 64 : 32;
+  const int row_bytes = p.epi_cw * esz;
   cuuint64_t dims[2] = {static_cast<cuuint64_t>(p.ldy), static_cast<cuuint64_t>(rows)};
   cuuint64_t strides[1] = {static_cast<cuuint64_t>(p.ldy) * esz};
-  cuuint32_t box[2] = {32, 32};
+  cuuint32_t box[2] = {static_cast<cuuint32_t>(p.epi_cw), 32};
   cuuint32_t es[2] = {1, 1};
   CUresult r = d->tiled(&p.tmY, out_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
                         Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                        out_f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        row_bytes == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
                         CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "Y tensor map failed (%d)", (int)r);
   return TIR_B200_OK;
@@ -353,7 +358,7 @@ int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64
   if (accumulate && (p.bias || p.relu)) return TIR_B200_OK;
   if (bn < 32 || !(p.groups == 1 || p.cog % 32 == 0) || (accumulate && Yin != Y)) return TIR_B200_OK;
   if ((reinterpret_cast<uintptr_t>(Y) & 15) || (p.ldy * (out_f16 ? 2 : 4)) % 16) return TIR_B200_OK;
-  int rc = encode_y(p, Y, rows, out_f16);
+  int rc = encode_y(p, Y, rows, out_f16, bn);
   if (rc) return rc;
   p.store_mode = accumulate ? 2 : 1;
   return TIR_B200_OK;
@@ -990,11 +995,12 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
 
 // ------------------------------------------------------------------ DEP
 
-template <int K, int S>
+// Tile shape per output width: 128 threads = 4 channel vectors x (TC/T) columns
+// x (TR/R) rows; a narrow image (MobileNet-V2's 14x14 / 7x7 stages) gets a
+// narrower tile so the footprint is not mostly padding.
+template <int K, int S, int R, int T, int TR, int TC>
 int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
                     int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
-  // 128 threads = 4 channel vectors x (TC/T) columns x (TR/R) rows
-  constexpr int R = S == 1 ? 4 : 2, T = 2, TR = 8, TC = S == 1 ? 32 : 16;
   constexpr int FR = (TR - 1) * S + K, FC = (TC - 1) * S + K;
   tb::DepTileParams p;
   std::memset(&p, 0, sizeof p);
@@ -1053,8 +1059,14 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
                        (reinterpret_cast<uintptr_t>(X) % 16 == 0);
   if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 32 == 0 && g.k[1] == 3 && g.k[2] == 3 &&
       g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
-    return g.s[1] == 1 ? launch_dep_tile<3, 1>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream)
-                       : launch_dep_tile<3, 2>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+    const int64_t ow = g.out[2];
+    if (g.s[1] == 1) {
+      if (ow >= 24) return launch_dep_tile<3, 1, 4, 2, 8, 32>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+      if (ow >= 12) return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+      return launch_dep_tile<3, 1, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+    }
+    if (ow >= 12) return launch_dep_tile<3, 2, 2, 2, 8, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+    return launch_dep_tile<3, 2, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   }
   tb::DepParams p;
   p.X = reinterpret_cast<const __half*>(X);

@@ -67,6 +67,11 @@ SMALL = {
     # more tiles than resident blocks: exercises the second TMA ring slot (128-B aligned)
     "DEP_s2_ring": tb.Conv("DEP", n=8, in_dhw=(1, 112, 112), ci=96, co=96, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
                            groups=96),
+    # narrow-image tile variants (MobileNet-V2 14x14 / 7x7 stages)
+    "DEP_14": tb.Conv("DEP", n=3, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), p=(0, 1, 1), groups=64),
+    "DEP_7": tb.Conv("DEP", n=5, in_dhw=(1, 7, 7), ci=96, co=96, k=(1, 3, 3), p=(0, 1, 1), groups=96),
+    "DEP_s2_14": tb.Conv("DEP", n=3, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
+                         groups=64),
     "DEP_c12": tb.Conv("DEP", n=1, in_dhw=(1, 7, 7), ci=12, co=12, k=(1, 5, 5), p=(0, 2, 2), groups=12),
 }
 

@@ -61,7 +61,8 @@ def show(label, fn):
 
 
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 100352
-for K, N in ((64, 64), (64, 256), (256, 64)):
+KN = [tuple(map(int, a.split("x"))) for a in sys.argv[2:]] or [(64, 64), (64, 256), (256, 64)]
+for K, N in KN:
     A = torch.randn(M, K, device=dev).half()
     B = torch.randn(K, N, device=dev).half()
     bias = torch.randn(N, device=dev)
