@@ -316,7 +316,7 @@ def traffic_from_profiles(name):
 
 # ----------------------------------------------------------------------------- networks
 
-NET_BATCH = {"resnet50": 32, "mobilenet_v2": 64}  # per GPU (weak scaling: global = N x this)
+NET_BATCH = {"resnet50": 32, "mobilenet_v2": 64, "bert_large": 8}  # per GPU (weak scaling: global = N x this)
 
 
 def measure_nets(device, world, rank, dist, steps, names):
@@ -333,7 +333,7 @@ def measure_nets(device, world, rank, dist, steps, names):
         per_gpu = NET_BATCH[name]
         global_batch = per_gpu * world
         net, (lo, hi) = nets.build_shard(name, global_batch, rank, world)
-        dn = nets.DeviceNet(net, device)
+        dn = nets.device_net(net, device)
         dn.input.normal_()
         dn.capture()
         for _ in range(3):
@@ -354,15 +354,22 @@ def measure_nets(device, world, rank, dist, steps, names):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
         sec = ms / 1e3
-        out[name] = {
-            "images_per_s": round(global_batch * steps / sec, 1),
+        line = {
+            "samples_per_s": round(global_batch * steps / sec, 1),
             "tflops": round(net.flops * world * steps / sec / 1e12, 2),
             "ms_per_forward": round(ms / steps, 4),
-            "batch_per_gpu": per_gpu, "global_batch": global_batch, "image": net.input_shape[1],
+            "batch_per_gpu": per_gpu, "global_batch": global_batch,
             "launches_per_forward": nets.launches_per_forward(net),
             "sharding": f"batch across {world} GPU(s), no collective" if world > 1 else "single GPU",
             "dtype": "fp16 activations / fp32 accumulate",
+            "weights": "random init (no checkpoints offline)",
         }
+        if isinstance(net, nets.BertDef):
+            line.update(seq=net.seq, layers=net.layers, tokens_per_s=round(global_batch * net.seq * steps / sec, 1),
+                        graph="encoder stack (embedding lookup excluded)")
+        else:
+            line.update(image=net.input_shape[1], images_per_s=line["samples_per_s"])
+        out[name] = line
         del dn
         torch.cuda.empty_cache()
     return out
@@ -448,7 +455,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nets", action="store_true", help="skip the batch-sharded network forwards")
-    ap.add_argument("--nets", default="resnet50,mobilenet_v2")
+    ap.add_argument("--nets", default="resnet50,mobilenet_v2,bert_large")
     ap.add_argument("--profile", metavar="OP", help="eager launches of one op for ncu (no timing)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)

@@ -159,6 +159,30 @@ int tir_b200_layernorm(const uint16_t* X, uint16_t* Y, const float* gamma, const
 int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols, float scale,
                      void* stream);
 
+/* Y[c, r] = X[r, col0 + c] (fp16; rows % 8 == 0, ld_in / ld_out / col0 multiples of 8). */
+int tir_b200_transpose(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t ld_in, int64_t col0,
+                       int64_t cols, int64_t ld_out, void* stream);
+
+/* ---- batched GMM (attention: per-(sequence, head) problems over strided views) ----
+ * Problem z = z1 * z2n + z2 (0 <= z1 < z1n, 0 <= z2 < z2n) computes
+ *   C[cr + m, cc + n] = epilogue( sum_k A[ar + m, ac + k] * B[br + k, bc + n] )
+ * where A [a_rows, lda], B [b_rows, ldb] (N contiguous) and C [c_rows, ldc] are
+ * plain row-major fp16 (C fp16 or fp32) tensors and each of ar, ac, br, bc, cr,
+ * cc is base + z1 * step1 + z2 * step2 (elements). No copies of the strided
+ * per-head views are made. M % 128 == 0, K % 64 == 0 and N % 32 == 0 per
+ * problem; bias (if any) is indexed by the problem-local column n. */
+typedef struct {
+  int64_t z1n, z2n;
+  int64_t a_row[3], a_col[3]; /* base, per-z1 step, per-z2 step */
+  int64_t b_row[3], b_col[3];
+  int64_t c_row[3], c_col[3];
+} tir_b200_batch_desc;
+
+int tir_b200_gmm_batched(const uint16_t* A, int64_t a_rows, int64_t lda, const uint16_t* B,
+                         int64_t b_rows, int64_t ldb, void* C, int64_t c_rows, int64_t ldc, int64_t M,
+                         int64_t N, int64_t K, const tir_b200_batch_desc* batch, int out_f16,
+                         const tir_b200_epilogue* epi, void* stream);
+
 /* Frees the calling thread's cached device/pinned buffers. */
 void tir_b200_release_host_cache(void);
 

@@ -70,3 +70,29 @@ def forward(net, x: np.ndarray) -> np.ndarray:
         bufs[op.dst] = y if op.out_f32 else _f16(y)
     out = bufs[net.output]
     return out.reshape(out.shape[0], -1).numpy()
+
+
+def bert_forward(net, x: np.ndarray) -> np.ndarray:
+    """Hidden states after `net.layers` encoder layers (float64, with the device
+    graph's fp16 rounding points: QKV, K^T (exact), scores, probabilities,
+    context, every GEMM output and both LayerNorms)."""
+    import torch
+
+    f16 = _f16
+    t = lambda a: torch.from_numpy(a).to(torch.float64)  # noqa: E731
+    B, S, H, nh, dh = net.batch, net.seq, net.hidden, net.heads, net.head_dim
+    xh = t(np.asarray(x, np.float16))
+    for w in net.weights:
+        qkv = f16(xh @ t(w["w_qkv"]) + t(w["b_qkv"]))
+        q = qkv[:, :H].reshape(B, S, nh, dh).permute(0, 2, 1, 3)
+        k = qkv[:, H:2 * H].reshape(B, S, nh, dh).permute(0, 2, 1, 3)
+        v = qkv[:, 2 * H:].reshape(B, S, nh, dh).permute(0, 2, 1, 3)
+        scores = f16(q @ k.transpose(-1, -2))
+        p = f16(torch.softmax(scores / np.sqrt(dh), dim=-1))
+        ctx = f16((p @ v).permute(0, 2, 1, 3).reshape(B * S, H))
+        attn = f16(ctx @ t(w["w_o"]) + t(w["b_o"]) + xh)
+        x1 = f16(torch.nn.functional.layer_norm(attn, (H,), t(w["ln1_g"]), t(w["ln1_b"]), net.eps))
+        hid = f16(torch.nn.functional.gelu(x1 @ t(w["w_f1"]) + t(w["b_f1"])))
+        y = f16(hid @ t(w["w_f2"]) + t(w["b_f2"]) + x1)
+        xh = f16(torch.nn.functional.layer_norm(y, (H,), t(w["ln2_g"]), t(w["ln2_b"]), net.eps))
+    return xh.numpy()

@@ -15,6 +15,8 @@ from .api import (  # noqa: F401
     conv,
     conv_host,
     gmm,
+    gmm_batched,
+    transpose,
     gmm_host,
     launch_count,
     lib,

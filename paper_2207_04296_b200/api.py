@@ -98,6 +98,12 @@ class Conv:
         return replace(self, **kw)
 
 
+class BatchDesc(ctypes.Structure):
+    """tir_b200_batch_desc: per-problem coordinates base + z1*step1 + z2*step2."""
+    _fields_ = [("z1n", ctypes.c_int64), ("z2n", ctypes.c_int64)] + [
+        (f"{t}_{d}", ctypes.c_int64 * 3) for t in "abc" for d in ("row", "col")]
+
+
 class Epilogue(ctypes.Structure):
     """tir_b200_epilogue: optional per-column fp32 bias, fp16 residual, then an
     activation (include/tir_b200.h)."""
@@ -134,6 +140,9 @@ def lib() -> ctypes.CDLL:
         L.tir_b200_avgpool_global.argtypes = [vp, vp, i64, i64, i64, vp]
         L.tir_b200_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, ctypes.c_float, vp]
         L.tir_b200_softmax.argtypes = [vp, vp, i64, i64, ctypes.c_float, vp]
+        L.tir_b200_transpose.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp]
+        L.tir_b200_gmm_batched.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, i64, i64,
+                                           ctypes.POINTER(BatchDesc), i32, ctypes.POINTER(Epilogue), vp]
         L.tir_b200_conv_host_f32.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, i32]
         _lib = L
     return _lib
@@ -309,6 +318,40 @@ def softmax(X, scale: float = 1.0, Y=None, *, stream=None):
     _need(Y, torch.float16, (rows, cols), "Y")
     _check(lib().tir_b200_softmax(_ptr(X), _ptr(Y), rows, cols, scale, _stream(stream)))
     return Y
+
+
+def transpose(X, col0: int, cols: int, Y=None, *, stream=None):
+    """Y [cols, rows] = X[:, col0:col0+cols]^T for a row-major fp16 X [rows, ld]."""
+    torch = _torch()
+    rows, ld = X.shape
+    _need(X, torch.float16, (rows, ld), "X")
+    if Y is None:
+        Y = torch.empty((cols, rows), dtype=torch.float16, device=X.device)
+    _need(Y, torch.float16, (cols, Y.shape[1]), "Y")
+    _check(lib().tir_b200_transpose(_ptr(X), _ptr(Y), rows, ld, col0, cols, Y.shape[1], _stream(stream)))
+    return Y
+
+
+def gmm_batched(A, B, C, M: int, N: int, K: int, z: tuple, a: tuple, b: tuple, c: tuple, *,
+                out_f16: bool = True, bias=None, relu=False, residual=None, stream=None):
+    """Batched GMM over strided windows of 2-D tensors (include/tir_b200.h):
+    problem (z1, z2) computes C[cr + m, cc + n] = sum_k A[ar + m, ac + k] * B[br + k, bc + n],
+    each coordinate given as ((base, step1, step2) for rows, (base, step1, step2) for cols)."""
+    torch = _torch()
+    _need(A, torch.float16, A.shape, "A")
+    _need(B, torch.float16, B.shape, "B")
+    _need(C, torch.float16 if out_f16 else torch.float32, C.shape, "C")
+    d = BatchDesc()
+    d.z1n, d.z2n = z
+    for name, (rows, cols) in zip("abc", (a, b, c)):
+        getattr(d, f"{name}_row")[:] = rows
+        getattr(d, f"{name}_col")[:] = cols
+    epi = _epilogue(bias, relu, N, A.device, residual, tuple(C.shape))
+    _check(lib().tir_b200_gmm_batched(_ptr(A), A.shape[0], A.shape[1], _ptr(B), B.shape[0], B.shape[1],
+                                      _ptr(C), C.shape[0], C.shape[1], M, N, K, ctypes.byref(d),
+                                      int(out_f16), ctypes.byref(epi) if epi is not None else None,
+                                      _stream(stream)))
+    return C
 
 
 # ---------------------------------------------------------------- host buffers

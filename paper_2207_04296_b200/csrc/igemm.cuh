@@ -72,6 +72,14 @@ struct SubProb {
   int32_t o_st[3], o_b[3];    // output coordinate = idx*st + b (x, y, z)
 };
 
+// Batched GMM (attention): problem z = z1 * z2n + z2 reads A_z[m, k] =
+// A[ar(z) + m, ac(z) + k], B_z[k, n] = B[br(z) + k, bc(z) + n] and writes
+// C_z[m, n] = C[cr(z) + m, cc(z) + n], each coordinate base + z1*step1 + z2*step2
+// over plain 2-D tensor maps (strided heads / batches need no copies).
+struct BatchAxis {
+  int32_t row[3], col[3];  // base, per-z1 step, per-z2 step
+};
+
 struct alignas(64) IgemmParams {
   CUtensorMap tmA[kMaxSub];
   CUtensorMap tmB;
@@ -106,7 +114,28 @@ struct alignas(64) IgemmParams {
   int32_t reduce;      // generic path: red.global.add into Y instead of stores (split-K)
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
+  int32_t batch_tiles;  // batched GMM: tiles per problem (0 = not batched)
+  int32_t batch_z2;     // problems per z1
+  BatchAxis ba, bb, bc; // A / B / C coordinates per problem
 };
+
+// Splits a batched tile id into (problem-local tile, z1, z2).
+__device__ __forceinline__ void split_batch(const IgemmParams& p, int& tile, int& z1, int& z2) {
+  z1 = z2 = 0;
+  if (p.batch_tiles) {
+    const int z = tile / p.batch_tiles;
+    tile -= z * p.batch_tiles;
+    z1 = z / p.batch_z2;
+    z2 = z - z1 * p.batch_z2;
+  }
+}
+
+__device__ __forceinline__ int batch_row(const BatchAxis& a, int z1, int z2) {
+  return a.row[0] + z1 * a.row[1] + z2 * a.row[2];
+}
+__device__ __forceinline__ int batch_col(const BatchAxis& a, int z1, int z2) {
+  return a.col[0] + z1 * a.col[1] + z2 * a.col[2];
+}
 
 template <int BN, int KS>
 struct IgemmCfg {
@@ -290,8 +319,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slot = 0, phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt, ks;
-      decompose_tile(p, tile, s, mt, g, nt, ks);
+      int s, mt, g, nt, ks, z1, z2, lt = tile;
+      split_batch(p, lt, z1, z2);
+      decompose_tile(p, lt, s, mt, g, nt, ks);
+      const int a_r = batch_row(p.ba, z1, z2), a_c = batch_col(p.ba, z1, z2);
+      const int b_r = batch_row(p.bb, z1, z2), b_c = batch_col(p.bb, z1, z2);
       const SubProb& sp = p.sub[s];
       const CUtensorMap* tmA = &p.tmA[s];
       const int m0 = mt * kBM;
@@ -321,7 +353,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int pc = st * pps + j;
             void* dA = sA + j * piece_bytes;
             if (a_mode == A_TILED) {
-              tma_load_2d(dA, tmA, &full[slot], pc * kBK, m0);
+              tma_load_2d(dA, tmA, &full[slot], pc * kBK + a_c, m0 + a_r);
               continue;
             }
             // Past the last piece: re-read the last real A piece (finite data)
@@ -350,8 +382,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
             for (int ch = 0; ch < kBChunks; ++ch)
               if ((pps + ch) % kProducers == pw)
-                tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk,
-                            st * Cfg::kBRows);
+                tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk + b_c,
+                            st * Cfg::kBRows + b_r);
           }
           if (trace && pw == 0 && it < 128) trace[2 * it + 1] = clock64();
         }
@@ -402,8 +434,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t slot = 0, phase = 0, acc = 0, acc_phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt, ks;
-      decompose_tile(p, tile, s, mt, g, nt, ks);
+      int s, mt, g, nt, ks, z1, z2, lt = tile;
+      split_batch(p, lt, z1, z2);
+      decompose_tile(p, lt, s, mt, g, nt, ks);
       int st0, st1;
       split_range(p, p.sub[s].num_stages, ks, st0, st1);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
@@ -463,16 +496,20 @@ __global__ void __launch_bounds__(kThreads, 1)
       const bool epi_on = p.bias || p.relu || p.residual;
       int local = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
-        int s, mt, g, nt;
-        decompose_tile(p, tile, s, mt, g, nt);
-        const int64_t row = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
-        const int64_t col_tile = static_cast<int64_t>(g) * p.cog + nt * BN;
+        int s, mt, g, nt, z1, z2, lt = tile;
+        split_batch(p, lt, z1, z2);
+        decompose_tile(p, lt, s, mt, g, nt);
+        const int c_r = batch_row(p.bc, z1, z2), c_c = batch_col(p.bc, z1, z2);
+        const int64_t row_local = static_cast<int64_t>(mt) * kBM + q * 32 + lane;
+        const int64_t row = row_local + c_r;  // row of the C tensor
+        const int64_t colb_tile = static_cast<int64_t>(g) * p.cog + nt * BN;  // bias column (per problem)
+        const int64_t col_tile = colb_tile + c_c;                               // column of the C tensor
         const int valid_tile = p.cog - nt * BN;  // columns of this tile inside the group
         // bias of the next 32 columns, one column per lane (prefetched a chunk ahead)
-        float bnext = (p.bias && static_cast<int>(lane) < valid_tile) ? __ldg(p.bias + col_tile + lane) : 0.0f;
+        float bnext = (p.bias && static_cast<int>(lane) < valid_tile) ? __ldg(p.bias + colb_tile + lane) : 0.0f;
         // residual rows past M are clipped by the TMA store and never read
-        const uint16_t* res_row = (p.residual && row < p.sub[0].m_count) ? p.residual + row * p.ldy + col_tile
-                                                                         : nullptr;
+        const uint16_t* res_row = (p.residual && row_local < p.sub[0].m_count)
+                                      ? p.residual + row * p.ldy + col_tile : nullptr;
         uint4 rp[4];  // fp16 residual of the next 32 columns
         auto fetch_res = [&](int c) {
           if (res_row && valid_tile - c >= 32 && (reinterpret_cast<uintptr_t>(res_row + c) & 15) == 0) {
@@ -504,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               if (p.bias) {
                 const float bcur = bnext;
                 const int nc = cc + 32 + static_cast<int>(lane);
-                bnext = nc < valid_tile ? __ldg(p.bias + col_tile + nc) : 0.0f;
+                bnext = nc < valid_tile ? __ldg(p.bias + colb_tile + nc) : 0.0f;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bcur, i);
               }
@@ -559,7 +596,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           __syncwarp();
           if (lane == 0) {
             const int col = static_cast<int>(col_tile) + c0;
-            const int row0 = mt * kBM + static_cast<int>(q) * 32;
+            const int row0 = mt * kBM + static_cast<int>(q) * 32 + c_r;
             if (p.store_mode == 2) tma_reduce_add_2d(&p.tmY, buf, col, row0);
             else tma_store_2d(&p.tmY, buf, col, row0);
             tma_store_commit();

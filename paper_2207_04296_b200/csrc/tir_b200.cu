@@ -244,7 +244,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   int grid = std::min(p.total_tiles, di.sms);
   // Keep B resident when its whole K panel fits next to a >= 3-deep A ring and
   // every CTA can be pinned to one (group, n-tile): grid a multiple of `keys`.
-  if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && keys <= di.sms &&
+  if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && !p.batch_tiles && keys <= di.sms &&
       res_rows * Cfg::kBRowBytes < (1 << 18) && res_bytes + 3 * Cfg::kABytes <= budget) {
     p.b_mode = tb::B_RESIDENT;
     p.b_res_rows = res_rows;
@@ -514,6 +514,90 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
   if (rc) return rc;
   rc = prepare_split_output(p, C, Cin, M * N, accumulate, stream);
   if (rc) return rc;
+  return launch_igemm(p, bn, ks_eff, stream);
+}
+
+// ------------------------------------------------------------------ batched GMM
+
+int gmm_batched_impl(const uint16_t* A, int64_t a_rows, int64_t lda, const uint16_t* B, int64_t b_rows,
+                     int64_t ldb, void* C, int64_t c_rows, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                     const tir_b200_batch_desc* bt, int out_f16, const Epi& epi, cudaStream_t stream) {
+  if (!A || !B || !C || !bt) return set_err(TIR_B200_ERR_VALUE, "gmm_batched: null operand");
+  if (M <= 0 || N <= 0 || K <= 0 || bt->z1n <= 0 || bt->z2n <= 0)
+    return set_err(TIR_B200_ERR_VALUE, "gmm_batched: empty problem");
+  if (M % tb::kBM || K % tb::kBK || N % 32)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: needs M %% 128 == 0, K %% 64 == 0, N %% 32 == 0");
+  if (lda % 8 || ldb % 8 || ldc % 8)
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: leading dims must be multiples of 8");
+  if (epi.residual && !out_f16) return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: residual needs fp16 C");
+  // every problem's windows inside their tensors (checked at the z corners; coordinates are affine in z)
+  const int64_t lim[3][2] = {{a_rows - M, lda - K}, {b_rows - K, ldb - N}, {c_rows - M, ldc - N}};
+  const int64_t* ax[3][2] = {{bt->a_row, bt->a_col}, {bt->b_row, bt->b_col}, {bt->c_row, bt->c_col}};
+  for (int t = 0; t < 3; ++t)
+    for (int d = 0; d < 2; ++d)
+      for (int64_t z1 : {int64_t(0), bt->z1n - 1})
+        for (int64_t z2 : {int64_t(0), bt->z2n - 1}) {
+          const int64_t v = ax[t][d][0] + z1 * ax[t][d][1] + z2 * ax[t][d][2];
+          if (v < 0 || v > lim[t][d] || v >= (1ll << 31))
+            return set_err(TIR_B200_ERR_VALUE, "gmm_batched: operand %d window out of bounds", t);
+        }
+  const DeviceInfo di = device_info();
+  tb::IgemmParams p;
+  std::memset(&p, 0, sizeof p);
+  int bn = 256;
+  while (bn > 32 && N % bn) bn /= 2;
+  const int64_t tiles_m = M / tb::kBM;
+  const int64_t probs = bt->z1n * bt->z2n;
+  while (bn > 32 && probs * tiles_m * (N / bn) < di.sms) bn /= 2;  // fill the machine
+  const int ks = choose_ks(static_cast<int>(K / 64), 64, bn);
+  const int ks_eff = bn >= 128 ? std::min(ks, 2) : ks;
+  int rc = encode_2d(&p.tmA[0], A, a_rows, lda, 64, tb::kBM);
+  if (rc) return rc;
+  rc = encode_2d(&p.tmB, B, b_rows, ldb, std::min(bn, 64), tb::kBK * ks_eff);
+  if (rc) return rc;
+  p.num_sub = 1;
+  tb::SubProb& s = p.sub[0];
+  set_sub_identity(s);
+  s.m_count = static_cast<int32_t>(M);
+  s.gx = static_cast<int32_t>(M);
+  s.gy = s.gz = 1;
+  s.num_pieces = static_cast<int32_t>(K / 64);
+  p.groups = 1;
+  p.a_mode = tb::A_TILED;
+  p.a_box_ch = 64;
+  p.cig = static_cast<int32_t>(K);
+  p.cb_per_tap = s.num_pieces;
+  p.b_mode = tb::B_STREAM;
+  p.k_rows = static_cast<int32_t>(b_rows);
+  p.w_kx = p.w_ky = 1;
+  p.cog = static_cast<int32_t>(N);
+  p.ldy = static_cast<int32_t>(ldc);
+  p.out_dims[0] = static_cast<int32_t>(M);
+  p.out_dims[1] = p.out_dims[2] = 1;
+  p.out_f16 = out_f16;
+  p.Y = C;
+  epi.apply(p);
+  p.ksplit = 1;
+  rc = finalize_tiles(p, bn, ks_eff);
+  if (rc) return rc;
+  p.batch_tiles = p.total_tiles;
+  p.batch_z2 = static_cast<int32_t>(bt->z2n);
+  if (static_cast<int64_t>(p.total_tiles) * probs >= (1ll << 31))
+    return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: too many tiles");
+  p.total_tiles = static_cast<int32_t>(p.total_tiles * probs);
+  auto axis = [](tb::BatchAxis& a, const int64_t* r, const int64_t* c) {
+    for (int i = 0; i < 3; ++i) {
+      a.row[i] = static_cast<int32_t>(r[i]);
+      a.col[i] = static_cast<int32_t>(c[i]);
+    }
+  };
+  axis(p.ba, bt->a_row, bt->a_col);
+  axis(p.bb, bt->b_row, bt->b_col);
+  axis(p.bc, bt->c_row, bt->c_col);
+  // TMA-store epilogue over the whole C tensor (per-problem coordinates)
+  rc = pick_store_mode(p, bn, C, nullptr, c_rows, 0, out_f16);
+  if (rc) return rc;
+  if (p.store_mode != 1) return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: C must be 16-byte aligned");
   return launch_igemm(p, bn, ks_eff, stream);
 }
 
@@ -1397,6 +1481,29 @@ int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols,
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return TIR_B200_OK;
+}
+
+int tir_b200_transpose(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t ld_in, int64_t col0, int64_t cols,
+                       int64_t ld_out, void* stream) {
+  int rc = check_vec(X, Y, 8);
+  if (rc) return rc;
+  if (rows <= 0 || cols <= 0 || rows % 8 || ld_in % 8 || ld_out % 8 || col0 % 8 || col0 + cols > ld_in ||
+      rows > ld_out || rows >= (1ll << 31) || cols >= (1ll << 31))
+    return set_err(TIR_B200_ERR_VALUE, "transpose: bad geometry");
+  dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
+  tb::transpose_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(X, Y, (int)rows, (int)ld_in, (int)col0,
+                                                                          (int)cols, (int)ld_out);
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+int tir_b200_gmm_batched(const uint16_t* A, int64_t a_rows, int64_t lda, const uint16_t* B, int64_t b_rows,
+                         int64_t ldb, void* C, int64_t c_rows, int64_t ldc, int64_t M, int64_t N, int64_t K,
+                         const tir_b200_batch_desc* batch, int out_f16, const tir_b200_epilogue* epi,
+                         void* stream) {
+  return gmm_batched_impl(A, a_rows, lda, B, b_rows, ldb, C, c_rows, ldc, M, N, K, batch, out_f16,
+                          make_epi(epi), static_cast<cudaStream_t>(stream));
 }
 
 void tir_b200_release_host_cache(void) {

@@ -230,8 +230,11 @@ class DeviceNet:
             self.graph.replay()
 
 
-def launches_per_forward(net: NetDef) -> int:
-    """Kernel launches of one forward (CI % 8 != 0 stems add the two relayout kernels)."""
+def launches_per_forward(net) -> int:
+    """Kernel launches of one forward (CI % 8 != 0 stems add the two relayout kernels;
+    a BERT layer is 10 launches)."""
+    if isinstance(net, BertDef):
+        return 10 * net.layers
     n = 0
     for op in net.ops:
         n += 1
@@ -241,8 +244,146 @@ def launches_per_forward(net: NetDef) -> int:
 
 
 def build_shard(name: str, global_batch: int, rank: int, world: int, **kw):
-    """(NetDef of this rank's samples, (lo, hi)) — same seed, so weights are replicated."""
+    """(net definition of this rank's samples, (lo, hi)) — same seed, so weights are replicated."""
     from . import shard
 
     lo, hi = shard.batch_range(global_batch, rank, world)
     return NETS[name](hi - lo, **kw), (lo, hi)
+
+
+# ---------------------------------------------------------------------- BERT
+
+@dataclass
+class BertDef:
+    """BERT encoder stack (post-LN, GELU FFN) on fp16 hidden states [B*S, H]:
+    per layer QKV GEMM (+bias) -> K^T relayout -> batched Q K^T over (sequence,
+    head) -> softmax(scale) -> batched P V -> output GEMM (+bias +residual) ->
+    LayerNorm -> FFN GEMM (+bias, GELU) -> GEMM (+bias +residual) -> LayerNorm.
+    The token embedding lookup is not part of the operator graph: the input is
+    the embedded hidden-state tensor."""
+
+    name: str
+    batch: int
+    seq: int = 512
+    hidden: int = 1024
+    heads: int = 16
+    ffn: int = 4096
+    layers: int = 24
+    eps: float = 1e-12
+    weights: list = field(default_factory=list)  # per layer dict of host arrays
+
+    @property
+    def tokens(self):
+        return self.batch * self.seq
+
+    @property
+    def head_dim(self):
+        return self.hidden // self.heads
+
+    @property
+    def input_shape(self):
+        return (self.tokens, self.hidden)
+
+    @property
+    def flops(self):
+        t, h, f, s = self.tokens, self.hidden, self.ffn, self.seq
+        dense = 2 * t * (3 * h * h + h * h + 2 * h * f)
+        attn = 2 * 2 * self.batch * self.heads * s * s * self.head_dim
+        return self.layers * (dense + attn)
+
+
+def bert_large(batch: int, seq: int = 512, layers: int = 24, hidden: int = 1024, heads: int = 16,
+               ffn: int = 4096, seed: int = 0) -> BertDef:
+    rng = np.random.default_rng(seed)
+    net = BertDef("bert_large", batch, seq, hidden, heads, ffn, layers)
+    for _ in range(layers):
+        w = {}
+        for key, (k, n) in (("qkv", (hidden, 3 * hidden)), ("o", (hidden, hidden)), ("f1", (hidden, ffn)),
+                            ("f2", (ffn, hidden))):
+            w["w_" + key] = (rng.standard_normal((k, n)) * (0.5 / math.sqrt(k))).astype(np.float16)
+            w["b_" + key] = (rng.standard_normal(n) * 0.02).astype(np.float32)
+        for ln in ("ln1", "ln2"):
+            w[ln + "_g"] = (1.0 + 0.1 * rng.standard_normal(hidden)).astype(np.float32)
+            w[ln + "_b"] = (0.1 * rng.standard_normal(hidden)).astype(np.float32)
+        net.weights.append(w)
+    return net
+
+
+NETS["bert_large"] = bert_large
+
+
+class DeviceBert:
+    """BertDef on one GPU: device weights, shared activation buffers, CUDA-graph forward."""
+
+    def __init__(self, net: BertDef, device):
+        import torch
+
+        self.net = net
+        self.device = device
+        t, h, f = net.tokens, net.hidden, net.ffn
+        e = lambda *s: torch.empty(s, dtype=torch.float16, device=device)  # noqa: E731
+        self.x = e(t, h)          # layer input / output (hidden states)
+        self.qkv = e(t, 3 * h)
+        self.kt = e(h, t)         # K^T: [hidden, tokens]
+        self.scores = e(net.batch * net.heads * net.seq, net.seq)
+        self.ctx = e(t, h)
+        self.attn = e(t, h)
+        self.x1 = e(t, h)
+        self.hid = e(t, f)
+        self.y = e(t, h)
+        self.w = [{k: torch.from_numpy(v).to(device) for k, v in lw.items()} for lw in net.weights]
+        self.stream = torch.cuda.Stream(device=device)
+        self.graph = None
+
+    @property
+    def input(self):
+        return self.x
+
+    @property
+    def output(self):
+        return self.x
+
+    def run(self, lo: int = 0, hi: int | None = None):
+        net, st = self.net, self.stream
+        B, S, H, nh, dh = net.batch, net.seq, net.hidden, net.heads, net.head_dim
+        for li in range(lo, net.layers if hi is None else hi):
+            w = self.w[li]
+            api.gmm(self.x, w["w_qkv"], self.qkv, out_f16=True, bias=w["b_qkv"], stream=st)
+            api.transpose(self.qkv, H, H, self.kt, stream=st)
+            # scores[(b*nh + h)*S + m, n] = Q[b*S + m, h*dh + k] . K^T[h*dh + k, b*S + n]
+            api.gmm_batched(self.qkv, self.kt, self.scores, S, S, dh, (B, nh),
+                            a=((0, S, 0), (0, 0, dh)), b=((0, 0, dh), (0, S, 0)),
+                            c=((0, nh * S, S), (0, 0, 0)), stream=st)
+            api.softmax(self.scores, 1.0 / math.sqrt(dh), Y=self.scores, stream=st)
+            # ctx[b*S + m, h*dh + n] = P[(b*nh + h)*S + m, k] . V[b*S + k, 2H + h*dh + n]
+            api.gmm_batched(self.scores, self.qkv, self.ctx, S, dh, S, (B, nh),
+                            a=((0, nh * S, S), (0, 0, 0)), b=((0, S, 0), (2 * H, 0, dh)),
+                            c=((0, S, 0), (0, 0, dh)), stream=st)
+            api.gmm(self.ctx, w["w_o"], self.attn, out_f16=True, bias=w["b_o"], residual=self.x, stream=st)
+            api.layernorm(self.attn, w["ln1_g"], w["ln1_b"], net.eps, Y=self.x1, stream=st)
+            api.gmm(self.x1, w["w_f1"], self.hid, out_f16=True, bias=w["b_f1"], relu="gelu", stream=st)
+            api.gmm(self.hid, w["w_f2"], self.y, out_f16=True, bias=w["b_f2"], residual=self.x1, stream=st)
+            api.layernorm(self.y, w["ln2_g"], w["ln2_b"], net.eps, Y=self.x, stream=st)
+
+    def capture(self):
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            self.run()
+        self.stream.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
+            self.run()
+        self.graph = g
+        return g
+
+    def replay(self):
+        import torch
+
+        with torch.cuda.stream(self.stream):
+            self.graph.replay()
+
+
+def device_net(net, device):
+    """DeviceNet for conv graphs, DeviceBert for BERT."""
+    return DeviceBert(net, device) if isinstance(net, BertDef) else DeviceNet(net, device)

@@ -84,3 +84,25 @@ def test_two_rank_gloo_network_shard(tmp_path):
            "--master-addr", "127.0.0.1", "--master-port", "29541", str(script)]
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env)
     assert "NET_SHARD_OK" in p.stdout, p.stdout + p.stderr
+
+
+def test_bert_structure_and_flops():
+    net = nets.bert_large(1, seq=512)
+    assert net.layers == 24 and net.hidden == 1024 and net.heads == 16 and net.head_dim == 64
+    # ~335 M parameters in the encoder stack's GEMMs (24 x 12.6 M)
+    params = sum(v.size for w in net.weights for k, v in w.items() if k.startswith("w_"))
+    assert abs(params / 24 / 12.58e6 - 1) < 0.01
+    # per 512-token sequence: dense 2 x 512 x 12.58M x 24 + attention 4 x 16 x 512^2 x 64 x 24
+    assert net.flops == 24 * (2 * 512 * (4 * 1024 * 1024 + 2 * 1024 * 4096) + 4 * 16 * 512 * 512 * 64)
+    assert nets.launches_per_forward(net) == 240
+
+
+def test_bert_reference_small():
+    from oracle import nets_ref
+
+    net = nets.bert_large(2, seq=128, layers=2, hidden=128, heads=2, ffn=512)
+    x = np.random.default_rng(0).standard_normal(net.input_shape).astype(np.float16)
+    y = nets_ref.bert_forward(net, x)
+    assert y.shape == net.input_shape and np.isfinite(y).all()
+    # post-LN output: every token row normalised (then scaled by ~1 gamma)
+    assert np.abs(y.mean(axis=1)).max() < 0.5
