@@ -660,25 +660,25 @@ int pick_box(int64_t cig) {
 
 constexpr int kNotEligible = -100;  // halo path declines; caller uses im2col
 
-template <int BN, int KH, int KW>
+template <int BN, int KH, int KW, bool TAPN = false>
 int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
-  using Cfg = tb::HaloCfg<BN>;
+  using Cfg = tb::HaloCfg<BN, TAPN>;
   const DeviceInfo di = device_info();
   const int keys = p.groups * p.tiles_n;
   if (keys > di.sms) return kNotEligible;
   if (BN > 64 && p.b_rows * Cfg::kBRowBytes >= (1 << 18)) return kNotEligible;
-  const int fixed = 1024 + 256 + p.b_rows * BN * 2 + 2 * p.stage_bytes;
+  const int fixed = 1024 + 256 + p.b_rows * BN * 2 + 2 * p.stage_bytes + Cfg::kXchBytes;
   const int slab = p.slab_rows * 128;
   const int stages = std::min(4, (di.smem_optin - fixed) / slab);
   if (stages < 2) return kNotEligible;
   p.stages = stages;
   const size_t smem = Cfg::smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW, TAPN>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int grid = std::min(p.total_tiles, di.sms / keys * keys);
   if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
   p.trace = g_trace;
-  CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW>, grid, tb::kHaloThreads, smem, stream, p));
+  CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW, TAPN>, grid, tb::kHaloThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
 }
@@ -831,6 +831,14 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
     }
   }
   const bool k3 = KH == 3 && KW == 3;
+  // Tap-packed N (halo.cuh): 3x3 undilated, 64-column tiles, TMA-store epilogue.
+  // Opt-in (TIR_B200_TAPN=1): measured on B200 it cuts the MMA time per C2D tile
+  // from ~2500 to ~1150 cycles, but reading the 3x wider accumulator out of TMEM
+  // (~1000 cycles per tile) plus the row-shift adds make the epilogue the
+  // limiter (13.6 vs 9.6 us for the paper shape).
+  if (k3 && d == 1 && bn == 64 && !linear && (p.store_mode == 1 || p.store_mode == 2) &&
+      getenv("TIR_B200_TAPN"))
+    return launch_halo_bn<64, 3, 3, true>(p, stream);
   switch (bn) {
     case 16: return k3 ? launch_halo_bn<16, 3, 3>(p, stream) : launch_halo_bn<16, 0, 0>(p, stream);
     case 32: return k3 ? launch_halo_bn<32, 3, 3>(p, stream) : launch_halo_bn<32, 0, 0>(p, stream);

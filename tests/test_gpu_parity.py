@@ -252,3 +252,27 @@ def test_native_kernels_actually_launch(cuda):
             torch.zeros(*spec.w_shape(), device=cuda, dtype=torch.float16))
     torch.cuda.synchronize()
     assert tb.launch_count() == 2
+
+
+@pytest.mark.parametrize("variant", ["TIR_B200_TAPN", "TIR_B200_HALO_LINEAR"])
+def test_opt_in_halo_variants_exact(variant, monkeypatch, cuda):
+    """The measured-and-rejected halo variants (tap-packed N, linear tiles) stay
+    correct: bit-exact on the reference distribution, with bias + ReLU and fp16
+    output, at the paper's C2D shape (sampled images) and a small wide shape."""
+    monkeypatch.setenv(variant, "1")
+    import torch
+
+    for spec in (tb.PAPER_SHAPES["C2D"], tb.Conv("C2D", n=2, in_dhw=(1, 5, 140), ci=64, co=64, k=(1, 3, 3),
+                                                  p=(0, 1, 1))):
+        x = O.reference_tensor(spec.x_shape(), 21)
+        w = O.reference_tensor(spec.w_shape(), 22)
+        bias = O.reference_tensor((spec.co,), 23)
+        got = run_conv(spec, x, w, cuda)
+        fused = tb.conv(spec, dev(x, cuda), dev(w, cuda), out_f16=True, bias=torch.from_numpy(bias).to(cuda),
+                        relu=True).float().cpu().numpy()
+        one = ospec(spec.with_(n=1))
+        for img in (0, spec.n - 1):
+            want = O.conv(one, x[img:img + 1], w, threads=8)
+            assert O.tensors_bitwise_equal(got[img:img + 1], want), (variant, img)
+            ref16 = np.maximum(want + bias, 0).astype(np.float16).astype(np.float32)
+            assert np.array_equal(fused[img:img + 1], ref16), (variant, img)

@@ -51,6 +51,11 @@ def show(name, fn):
             by_tiles.setdefault(nt, []).append(e)
         for nt, es in sorted(by_tiles.items()):
             print(f"  CTAs with {nt} tiles: {len(es)}, end ns min {min(es)} max {max(es)}")
+    for i in range(8):
+        w = t[1536 + 8 * i: 1543 + 8 * i]
+        if w[0] == 0:
+            break
+        print("tapn epi tile %d: start %7d tfull %7d ld+arrive %7d xbar %7d pre-stage %7d stage-bar %7d stored %7d" % (i, *(x - t0 for x in w)))
     for i in range(64):
         a, b = t[512 + 2 * i], t[513 + 2 * i]
         if a == 0:
