@@ -10,6 +10,8 @@
 //    value that does not survive the round trip (rejected as ValueError).
 #pragma once
 
+#include <algorithm>
+
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -102,6 +104,90 @@ __global__ void pack_kw_weights_kernel(const uint16_t* __restrict__ w, uint16_t*
     const int32_t j = static_cast<int32_t>(row - g * cp);
     y[i] = j < kwc ? w[(g * kwc + j) * co + col] : static_cast<uint16_t>(0);
   }
+}
+
+// (kw, c) packing of X and of the weights in ONE launch (replaces the two
+// kernels above on the hot path). Blocks [0, rows) each relayout one input row
+// (n, d, h): the row (iw * c halves, <= 48 KB) is staged in shared memory with
+// 16-byte loads, then every 16-byte output vector (o, 8 packed channels) is
+// gathered from it; per-row indices stay 32-bit and the (t, ch) split of a
+// packed channel comes from a small table (the old per-element int64 div/mod
+// made the relayout run at 1.5 TB/s). Blocks [rows, rows + wblocks) pack the
+// weights [khd][kwc][co] -> [khd][cp][co] (zero rows j >= kwc).
+__global__ void __launch_bounds__(256) pack_kw_fused_kernel(
+    const uint16_t* __restrict__ x, uint16_t* __restrict__ y, const uint16_t* __restrict__ w,
+    uint16_t* __restrict__ wy, int32_t rows, int32_t rpb, int32_t xblocks, int32_t iw, int32_t c, int32_t ow,
+    int32_t kw, int32_t sw, int32_t pw, int32_t dw, int32_t cp, int32_t khd, int32_t kwc, int32_t co) {
+  extern __shared__ __align__(16) uint16_t srow[];  // rpb staged input rows
+  __shared__ int16_t tab_t[64], tab_c[64];
+  if (static_cast<int32_t>(blockIdx.x) >= xblocks) {  // weights
+    const int64_t total = static_cast<int64_t>(khd) * cp * co;
+    const int64_t step = static_cast<int64_t>(gridDim.x - xblocks) * blockDim.x;
+    for (int64_t i = (blockIdx.x - xblocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += step) {
+      const int32_t col = static_cast<int32_t>(i % co);
+      const int64_t r = i / co;
+      const int32_t g = static_cast<int32_t>(r / cp), j = static_cast<int32_t>(r % cp);
+      wy[i] = j < kwc ? w[(static_cast<int64_t>(g) * kwc + j) * co + col] : static_cast<uint16_t>(0);
+    }
+    return;
+  }
+  if (threadIdx.x < cp) {
+    tab_t[threadIdx.x] = static_cast<int16_t>(threadIdx.x / c);
+    tab_c[threadIdx.x] = static_cast<int16_t>(threadIdx.x % c);
+  }
+  const int32_t row0 = blockIdx.x * rpb;
+  const int32_t nrows = min(rpb, rows - row0);
+  const int32_t row_elems = iw * c;
+  const uint16_t* xr = x + static_cast<int64_t>(row0) * row_elems;
+  // all rows of the block in flight at once (the loads are the latency-bound half)
+  if ((row_elems & 7) == 0 && (reinterpret_cast<uintptr_t>(xr) & 15) == 0) {
+    for (int v = threadIdx.x; v < nrows * row_elems / 8; v += blockDim.x)
+      reinterpret_cast<uint4*>(srow)[v] = __ldg(reinterpret_cast<const uint4*>(xr) + v);
+  } else {
+    for (int v = threadIdx.x; v < nrows * row_elems; v += blockDim.x) srow[v] = __ldg(xr + v);
+  }
+  __syncthreads();
+  const int32_t gshift = cp == 8 ? 0 : cp == 16 ? 1 : cp == 32 ? 2 : 3;  // log2(cp / 8)
+  const int32_t nvec = ow << gshift;
+  uint4* yb = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row0) * ow * cp);
+  for (int32_t v = threadIdx.x; v < nrows * nvec; v += blockDim.x) {
+    const int32_t r = v / nvec, vr = v - r * nvec;
+    const int32_t o = vr >> gshift, grp = vr & ((1 << gshift) - 1);
+    const int32_t base = o * sw - pw;
+    const uint16_t* sr = srow + r * row_elems;
+    uint16_t e8[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t j = grp * 8 + e;
+      const int32_t t = tab_t[j], ch = tab_c[j];
+      const int32_t wi = base + t * dw;
+      e8[e] = (t < kw && wi >= 0 && wi < iw) ? sr[wi * c + ch] : static_cast<uint16_t>(0);
+    }
+    uint4 u;
+    u.x = e8[0] | (static_cast<uint32_t>(e8[1]) << 16);
+    u.y = e8[2] | (static_cast<uint32_t>(e8[3]) << 16);
+    u.z = e8[4] | (static_cast<uint32_t>(e8[5]) << 16);
+    u.w = e8[6] | (static_cast<uint32_t>(e8[7]) << 16);
+    yb[v] = u;
+  }
+}
+
+inline int launch_pack_kw_fused(const uint16_t* x, uint16_t* y, const uint16_t* w, uint16_t* wy, int64_t rows,
+                                int64_t iw, int64_t c, int64_t ow, int64_t kw, int64_t sw, int64_t pw, int64_t dw,
+                                int64_t cp, int64_t khd, int64_t kwc, int64_t co, cudaStream_t st) {
+  const int64_t row_bytes = iw * c * 2;
+  if (row_bytes > 48 * 1024 || rows >= (1ll << 30) || cp > 64) return 2;  // caller falls back
+  const int rpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 12 * 1024 / row_bytes)));
+  const int64_t xblocks = (rows + rpb - 1) / rpb;
+  const int wblocks = 16;
+  const size_t smem = static_cast<size_t>(rpb * row_bytes + 16);
+  pack_kw_fused_kernel<<<static_cast<unsigned>(xblocks + wblocks), 256, smem, st>>>(
+      x, y, w, wy, static_cast<int32_t>(rows), rpb, static_cast<int32_t>(xblocks), static_cast<int32_t>(iw),
+      static_cast<int32_t>(c), static_cast<int32_t>(ow), static_cast<int32_t>(kw), static_cast<int32_t>(sw),
+      static_cast<int32_t>(pw), static_cast<int32_t>(dw), static_cast<int32_t>(cp), static_cast<int32_t>(khd),
+      static_cast<int32_t>(kwc), static_cast<int32_t>(co));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 inline int grid_for(int64_t n) {

@@ -873,12 +873,19 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     if (rc) return rc;
     uint16_t* Xp = static_cast<uint16_t*>(ws);
     uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
-    if (tb::launch_pack_kw(X, Xp, rows, g.in[2], cig, g.out[2], g.k[2], g.s[2], g.p[2], g.d[2], cp, stream))
-      return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
-    ++g_launches;
-    if (tb::launch_pack_kw_weights(W, Wp, khd, kwc, cp, g.co, stream))
-      return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
-    ++g_launches;
+    const int prc = tb::launch_pack_kw_fused(X, Xp, W, Wp, rows, g.in[2], cig, g.out[2], g.k[2], g.s[2], g.p[2],
+                                             g.d[2], cp, khd, kwc, g.co, stream);
+    if (prc == 1) return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+    if (prc == 0) {
+      ++g_launches;
+    } else {  // rows too long for the staged kernel: the two generic relayout kernels
+      if (tb::launch_pack_kw(X, Xp, rows, g.in[2], cig, g.out[2], g.k[2], g.s[2], g.p[2], g.d[2], cp, stream))
+        return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+      ++g_launches;
+      if (tb::launch_pack_kw_weights(W, Wp, khd, kwc, cp, g.co, stream))
+        return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+      ++g_launches;
+    }
     X = Xp;
     W = Wp;
     g.in[2] = g.out[2];
