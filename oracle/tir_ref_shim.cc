@@ -5,6 +5,7 @@
 // (/root/reference/proj/src/interp.cc:579-590) on programs written in the
 // reference grammar (parse_text, src/parser.cc:801). Built by oracle/Makefile
 // against the unmodified reference sources into oracle/_ref/.
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -132,6 +133,62 @@ const char* tirref_workload_source(const char* which, int a, int b, int c, int d
     return nullptr;
   }
   return src.c_str();
+}
+
+// The reference's tensor-file I/O (interp.cc:730-769), so golden vectors on
+// disk are written and read by the reference itself. dtype: "f32" / "f16" (f16
+// is stored as f32 bits, ir.cc:36-47).
+int tirref_write_tensor(const char* path, const char* dtype, int ndim, const int64_t* shape,
+                        const float* data) {
+  try {
+    std::string d(dtype);
+    tir::DType dt = d == "f16" ? tir::DType::F16 : tir::DType::F32;
+    tir::TensorValue t = tir::TensorValue::zeros(dt, std::vector<int64_t>(shape, shape + ndim));
+    std::memcpy(t.data.data(), data, t.data.size());
+    tir::write_tensor(path, t);
+    return 0;
+  } catch (const tir::Error& e) {
+    return fail(e.kind() + ": " + e.message());
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+
+// Reads a tensor file; returns the element count (or -1), the shape in
+// shape_out[0..*ndim) (at most 8 dims) and up to `cap` elements as f32.
+int64_t tirref_read_tensor(const char* path, float* out, int64_t cap, int64_t* shape_out, int* ndim) {
+  try {
+    tir::TensorValue t = tir::read_tensor(path);
+    if (!tir::dtype_is_float(t.dtype)) return fail("float tensors only");
+    *ndim = static_cast<int>(t.shape.size());
+    for (size_t i = 0; i < t.shape.size() && i < 8; ++i) shape_out[i] = t.shape[i];
+    const int64_t n = t.num_elements();
+    if (out) std::memcpy(out, t.data.data(), static_cast<size_t>(std::min(n, cap)) * 4);
+    return n;
+  } catch (const tir::Error& e) {
+    return fail(e.kind() + ": " + e.message());
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
+}
+
+// tir::run over inputs read from tensor files, first output written to a
+// tensor file: a golden vector produced end to end by the reference.
+int tirref_run_files(const char* ir_text, int n_in, const char* const* in_paths, const char* out_path) {
+  try {
+    tir::PrimFuncPtr f = tir::parse_text(ir_text);
+    std::vector<tir::TensorValue> values;
+    for (int i = 0; i < n_in; ++i) values.push_back(tir::read_tensor(in_paths[i]));
+    tir::ExecContext ctx;
+    auto outs = tir::run(*f, values, ctx);
+    if (outs.empty()) return fail("program has no output");
+    tir::write_tensor(out_path, outs[0]);
+    return 0;
+  } catch (const tir::Error& e) {
+    return fail(e.kind() + ": " + e.message());
+  } catch (const std::exception& e) {
+    return fail(e.what());
+  }
 }
 
 }  // extern "C"
