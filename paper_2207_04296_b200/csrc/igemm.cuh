@@ -611,7 +611,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           acc_phase ^= 1;
         }
       }
-      if (lane == 0) tma_store_wait_all<0>();
+      if (lane == 0) tma_store_wait_read<0>();  // smem reads done; the grid end flushes the writes
     } else {
       // Generic: TMEM -> registers (thread = output row) -> smem transpose ->
       // coalesced stores of 32-column row segments at per-row output offsets

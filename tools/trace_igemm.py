@@ -52,6 +52,13 @@ def show(name, fn):
         for nt, es in sorted(by_tiles.items()):
             print(f"  CTAs with {nt} tiles: {len(es)}, end ns min {min(es)} max {max(es)}")
     for i in range(8):
+        w = t[1600 + 8 * i: 1607 + 8 * i]
+        if w[0] == 0:
+            break
+        print("halo epi tile %d: ld_issue %7d ld_done %7d epi_done %7d buf_free %7d staged %7d bar2 %7d store_issued+wait1 %7d" % (i, *(x - t0 for x in w)))
+    if t[1599]:
+        print("epilogue final wait_read done %7d, after __syncthreads %7d" % (t[1599] - t0, t[1598] - t0))
+    for i in range(8):
         w = t[1536 + 8 * i: 1543 + 8 * i]
         if w[0] == 0:
             break
