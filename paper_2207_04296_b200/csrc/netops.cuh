@@ -195,6 +195,125 @@ __global__ void softmax_kernel(const uint16_t* __restrict__ X, uint16_t* __restr
   }
 }
 
+// Warp-per-row variants (cols <= 256 * VPL, the BERT shapes: 512-wide softmax
+// rows, 1024-wide LayerNorm rows): the row lives in one warp's registers,
+// reductions are shuffles, no block barriers, 8 rows per 256-thread block.
+__device__ __forceinline__ float warp_sum(float v) {
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) softmax_warp_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y,
+                                                           int rows, int cols, float scale) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int cv = cols / 8;
+  const uint4* x = reinterpret_cast<const uint4*>(X + static_cast<int64_t>(row) * cols);
+  float v[VPL][8];
+  float mx = -INFINITY;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < cv) {
+      H8 h;
+      h.u = __ldg(x + i);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(h.h[j]);
+        v[t][2 * j] = f.x * scale;
+        v[t][2 * j + 1] = f.y * scale;
+        mx = fmaxf(mx, fmaxf(v[t][2 * j], v[t][2 * j + 1]));
+      }
+    }
+  }
+  mx = warp_max(mx);
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    if (lane + 32 * t < cv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        v[t][j] = __expf(v[t][j] - mx);
+        sum += v[t][j];
+      }
+    }
+  }
+  const float inv = 1.0f / warp_sum(sum);
+  uint4* y = reinterpret_cast<uint4*>(Y + static_cast<int64_t>(row) * cols);
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i >= cv) continue;
+    H8 o;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o.h[j] = __floats2half2_rn(v[t][2 * j] * inv, v[t][2 * j + 1] * inv);
+    y[i] = o.u;
+  }
+}
+
+template <int VPL>
+__global__ void __launch_bounds__(256) layernorm_warp_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y,
+                                                             const float* __restrict__ gamma,
+                                                             const float* __restrict__ beta, int rows, int cols,
+                                                             float eps) {
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const int cv = cols / 8;
+  const uint4* x = reinterpret_cast<const uint4*>(X + static_cast<int64_t>(row) * cols);
+  float v[VPL][8];
+  float sum = 0.f;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i < cv) {
+      H8 h;
+      h.u = __ldg(x + i);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 f = __half22float2(h.h[j]);
+        v[t][2 * j] = f.x;
+        v[t][2 * j + 1] = f.y;
+        sum += f.x + f.y;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[t][j] = 0.f;
+    }
+  }
+  const float mean = warp_sum(sum) / cols;
+  float sq = 0.f;
+#pragma unroll
+  for (int t = 0; t < VPL; ++t)
+    if (lane + 32 * t < cv) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sq += (v[t][j] - mean) * (v[t][j] - mean);
+    }
+  const float rstd = rsqrtf(warp_sum(sq) / cols + eps);
+  uint4* y = reinterpret_cast<uint4*>(Y + static_cast<int64_t>(row) * cols);
+#pragma unroll
+  for (int t = 0; t < VPL; ++t) {
+    const int i = lane + 32 * t;
+    if (i >= cv) continue;
+    const float4 g0 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i);
+    const float4 g1 = __ldg(reinterpret_cast<const float4*>(gamma) + 2 * i + 1);
+    const float4 b0 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i);
+    const float4 b1 = __ldg(reinterpret_cast<const float4*>(beta) + 2 * i + 1);
+    const float g[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+    const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    H8 o;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      o.h[j] = __floats2half2_rn((v[t][2 * j] - mean) * rstd * g[2 * j] + b[2 * j],
+                                 (v[t][2 * j + 1] - mean) * rstd * g[2 * j + 1] + b[2 * j + 1]);
+    y[i] = o.u;
+  }
+}
+
 }  // namespace tb
 
 namespace tb {

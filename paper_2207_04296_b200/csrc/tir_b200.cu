@@ -1159,6 +1159,11 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
   if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 32 == 0 && g.k[1] == 3 && g.k[2] == 3 &&
       g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
     const int64_t ow = g.out[2];
+    const char* tc_env = getenv("TIR_B200_DEP_TC");  // tile-shape override (tuning)
+    if (g.s[1] == 1 && tc_env && atoi(tc_env) == 16)
+      return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+    if (g.s[1] == 1 && tc_env && atoi(tc_env) == 8)
+      return launch_dep_tile<3, 1, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
     if (g.s[1] == 1) {
       if (ow >= 24) return launch_dep_tile<3, 1, 4, 2, 8, 32>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
       if (ow >= 12) return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
@@ -1468,9 +1473,20 @@ int tir_b200_layernorm(const uint16_t* X, uint16_t* Y, const float* gamma, const
   if (cols > 8192 || rows < 0 || rows >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "layernorm: shape");
   if (rows == 0) return TIR_B200_OK;
   const int cv = static_cast<int>(cols / 8);
+  auto st = static_cast<cudaStream_t>(stream);
+  if ((reinterpret_cast<uintptr_t>(gamma) & 15) == 0 && (reinterpret_cast<uintptr_t>(beta) & 15) == 0 &&
+      cv <= 256) {  // warp per row
+    const unsigned gw = static_cast<unsigned>((rows + 7) / 8);
+    if (cv <= 32) tb::layernorm_warp_kernel<1><<<gw, 256, 0, st>>>(X, Y, gamma, beta, (int)rows, (int)cols, eps);
+    else if (cv <= 64) tb::layernorm_warp_kernel<2><<<gw, 256, 0, st>>>(X, Y, gamma, beta, (int)rows, (int)cols, eps);
+    else if (cv <= 128) tb::layernorm_warp_kernel<4><<<gw, 256, 0, st>>>(X, Y, gamma, beta, (int)rows, (int)cols, eps);
+    else tb::layernorm_warp_kernel<8><<<gw, 256, 0, st>>>(X, Y, gamma, beta, (int)rows, (int)cols, eps);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return TIR_B200_OK;
+  }
   const int threads = std::min(256, (cv + 31) / 32 * 32);
   const int vpt = (cv + threads - 1) / threads;
-  auto st = static_cast<cudaStream_t>(stream);
   const unsigned g = static_cast<unsigned>(rows);
   if (vpt == 1) tb::layernorm_kernel<1><<<g, threads, 0, st>>>(X, Y, gamma, beta, (int)cols, eps);
   else if (vpt == 2) tb::layernorm_kernel<2><<<g, threads, 0, st>>>(X, Y, gamma, beta, (int)cols, eps);
@@ -1486,9 +1502,19 @@ int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols,
   if (cols > 8192 || rows < 0 || rows >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "softmax: shape");
   if (rows == 0) return TIR_B200_OK;
   const int cv = static_cast<int>(cols / 8);
+  auto st = static_cast<cudaStream_t>(stream);
+  if (cv <= 256) {  // warp per row
+    const unsigned gw = static_cast<unsigned>((rows + 7) / 8);
+    if (cv <= 32) tb::softmax_warp_kernel<1><<<gw, 256, 0, st>>>(X, Y, (int)rows, (int)cols, scale);
+    else if (cv <= 64) tb::softmax_warp_kernel<2><<<gw, 256, 0, st>>>(X, Y, (int)rows, (int)cols, scale);
+    else if (cv <= 128) tb::softmax_warp_kernel<4><<<gw, 256, 0, st>>>(X, Y, (int)rows, (int)cols, scale);
+    else tb::softmax_warp_kernel<8><<<gw, 256, 0, st>>>(X, Y, (int)rows, (int)cols, scale);
+    CUDA_TRY(cudaGetLastError());
+    ++g_launches;
+    return TIR_B200_OK;
+  }
   const int threads = std::min(256, (cv + 31) / 32 * 32);
   const int vpt = (cv + threads - 1) / threads;
-  auto st = static_cast<cudaStream_t>(stream);
   const unsigned g = static_cast<unsigned>(rows);
   if (vpt == 1) tb::softmax_kernel<1><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
   else if (vpt == 2) tb::softmax_kernel<2><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
