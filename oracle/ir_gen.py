@@ -344,3 +344,53 @@ GMM_SHAPE = (1024, 1024, 1024)
 
 def small(spec: ConvSpec, **kw) -> ConvSpec:
     return replace(spec, **kw)
+
+
+def conv_source_direct(spec: ConvSpec, name: str | None = None) -> str:
+    """Forward, groups = 1 convolution with one loop per block iterator and
+    per-element read regions (A[vn +: 1, <input index> +: 1, ..., vrc +: 1]).
+    This is the form the reference's Schedule::pad_block accepts (trivial loop
+    bindings, directly indexed padded operands; schedule_block.cc:1186-1260),
+    used to express the channel pad CI -> multiple of 8 as IR steps
+    (cache_read + pad_block) instead of a device relayout."""
+    if spec.transposed or spec.groups != 1 or spec.op == "DEP":
+        raise ValueError("direct form: forward convolutions with groups == 1")
+    r = spec.spatial_rank
+    name = name or spec.op.lower()
+    out_sp = spec.out_dhw()[3 - r:]
+    in_sp, ks, ss, ps, ds = (t[3 - r:] for t in (spec.in_dhw, spec.k, spec.s, spec.p, spec.d))
+    sp = ["d", "h", "w"][3 - r:]
+    loops = [("n", spec.n)] + list(zip(sp, out_sp)) + [("co", spec.co)] + [(f"r{s}", k) for s, k in zip(sp, ks)] + \
+        [("rc", spec.ci)]
+    binds = [f"spatial vn: {spec.n} = n"] + [f"spatial v{s}: {e} = {s}" for s, e in zip(sp, out_sp)] + \
+        [f"spatial vco: {spec.co} = co"] + [f"reduce vr{s}: {k} = r{s}" for s, k in zip(sp, ks)] + \
+        [f"reduce vrc: {spec.ci} = rc"]
+    in_idx, conds = [], []
+    for s, I, s_, p_, d_ in zip(sp, in_sp, ss, ps, ds):
+        base = f"v{s}" if s_ == 1 else f"v{s}*{s_}"
+        tap = f"vr{s}" if d_ == 1 else f"vr{s}*{d_}"
+        idx = f"{base} + {tap}" + (f" - {p_}" if p_ else "")
+        in_idx.append(idx)
+        if p_ > 0:
+            conds += [f"{idx} >= 0", f"{idx} < {I}"]
+    a_idx = ", ".join(["vn", *in_idx, "vrc"])
+    y_idx = ", ".join(["vn", *[f"v{s}" for s in sp], "vco"])
+    w_idx = ", ".join([*[f"vr{s}" for s in sp], "vrc", "vco"])
+    region = lambda idx: ", ".join(f"{x} +: 1" for x in idx.split(", "))  # noqa: E731
+    a_load = f"f32(A[{a_idx}])"
+    if conds:
+        a_load = f"select({' and '.join(conds)}, {a_load}, 0.0)"
+    ind = "    "
+    lines = []
+    for depth, (v, e) in enumerate(loops):
+        lines.append(ind * depth + f"for {v} in 0..{e} {{")
+    depth = len(loops)
+    body = (f"block conv({', '.join(binds)}) reads(A[{region(a_idx)}], B[{region(w_idx)}]) "
+            f"writes(C[{region(y_idx)}]) {{\n  init {{\n    C[{y_idx}] = 0.0\n  }}\n"
+            f"  C[{y_idx}] = C[{y_idx}] + {a_load}*f32(B[{w_idx}])\n}}")
+    lines += [ind * depth + ln for ln in body.split("\n")]
+    for d in range(depth - 1, -1, -1):
+        lines.append(ind * d + "}")
+    header = (f"func {name}(A: f16[{_dims(None, spec.x_shape())}], B: f16[{_dims(None, spec.w_shape())}], "
+              f"C: f32[{_dims(None, spec.y_shape())}]) {{\n  block root() {{\n")
+    return header + "\n".join("    " + ln for ln in lines) + "\n  }\n}\n"

@@ -260,3 +260,20 @@ extern "C" int tir_b200_adapter_run_auto(const char* ir_text, const char* const*
     run_program(*s.func(), ctx, n_in, inputs, out, out_elems, intrinsic_calls);
   });
 }
+
+// Channel pad as IR steps (tir_b200_tensorize.h, pad_conv_channels): returns the
+// rewritten program and its trace (JSONL), after checking that replaying the trace
+// on a fresh parse reproduces it.
+extern "C" int tir_b200_adapter_pad_channels(const char* ir_text, const char* block, int64_t multiple, char* text,
+                                             int64_t text_len, char* trace, int64_t trace_len, int64_t* padded,
+                                             char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    tir::Schedule s(tir::parse_text(ir_text));
+    const int64_t p = tir_b200::pad_conv_channels(s, block, multiple);
+    tir::Schedule again = tir::replay(s.trace(), tir::parse_text(ir_text));
+    if (!tir::structural_equal(*again.func(), *s.func())) tir::throw_error("ReplayMismatch", "trace replay differs");
+    copy_out(tir::print_text(s.func()), text, text_len, "text");
+    copy_out(tir::trace_to_jsonl(s.trace()), trace, trace_len, "trace");
+    if (padded) *padded = p;
+  });
+}

@@ -451,6 +451,58 @@ void register_matched(tir::ExecContext& ctx, const OpMatch& m) {
   }
 }
 
+namespace {
+
+void widen_reads(tir::Schedule& s, const std::string& block) {
+  Stmt o = s.find_block_realize(block);
+  if (!o) tir::throw_error("StaleHandle", "no block named '" + block + "'");
+  auto blk = std::make_shared<tir::Block>(*o->block);
+  for (auto& r : blk->reads) {
+    r.ranges.clear();
+    for (int64_t d : r.buffer->shape) r.ranges.push_back(tir::const_range(0, d));
+  }
+  Stmt repl = tir::make_block_realize(o->bindings, o->predicate, blk);
+  Stmt body = rewrite(s.func()->body, o.get(), repl);
+  tir::TraceStep step;
+  step.prim = "b200.widen_reads";
+  step.args = {{"block", block}};
+  s.commit_rewrite(tir::make_func(s.func()->name, s.func()->params, body), std::move(step));
+}
+
+void register_widen_handler() {
+  static const bool registered = [] {
+    tir::register_step_handler("b200.widen_reads", [](tir::Schedule& s, const tir::TraceStep& step) {
+      widen_reads(s, step.args.at("block").get<std::string>());
+    });
+    return true;
+  }();
+  (void)registered;
+}
+
+}  // namespace
+
+int64_t pad_conv_channels(tir::Schedule& s, const std::string& block, int64_t multiple) {
+  register_widen_handler();
+  Stmt realize = s.find_block_realize(block);
+  if (!realize) tir::throw_error("StaleHandle", "no block named '" + block + "'");
+  const auto& ivs = realize->block->iter_vars;
+  std::vector<int64_t> ext(ivs.size());
+  int64_t padded = -1;
+  for (size_t i = 0; i < ivs.size(); ++i) {
+    if (!tir::as_const_int(ivs[i].domain.extent, &ext[i])) tir::throw_error("NotSchedulable", "non-constant domain");
+    if (var_name(ivs[i].var) == "vrc") {
+      padded = (ext[i] + multiple - 1) / multiple * multiple;
+      ext[i] = padded;
+    }
+  }
+  if (padded < 0) tir::throw_error("DescMismatch", "block '" + block + "' has no channel reduction 'vrc'");
+  s.cache_read(block, 0, "global");
+  s.cache_read(block, 1, "global");
+  s.pad_block(block, ext);
+  widen_reads(s, block);
+  return padded;
+}
+
 void register_tensorize_step_handler() {
   static const bool registered = [] {
     tir::register_step_handler("b200.tensorize", [](tir::Schedule& s, const tir::TraceStep& step) {

@@ -55,6 +55,21 @@ void register_matched(tir::ExecContext& ctx, const OpMatch& m);
 // Registers the replay handler for "b200.tensorize" trace steps (idempotent).
 void register_tensorize_step_handler();
 
+// the channel pad of small-CI convolutions (CI = 3 stems) as
+// reference schedule steps instead of a device relayout. On a conv block in the
+// direct form (one loop per iterator, per-element read regions):
+//   cache_read(block, 0), cache_read(block, 1)   -- stage X and W (schedule_block.cc:283)
+//   pad_block(block, rc -> padded)               -- grow the reduction to `padded`
+//                                                   channels, zero-filling the staged
+//                                                   copies (schedule_block.cc:1186)
+//   b200.widen_reads(block)                      -- declare whole-buffer read regions
+//                                                   (a conservative over-approximation)
+//                                                   so a later whole-op tensorize sees
+//                                                   in-bounds operand windows
+// Every step is recorded in the trace; the last one replays through
+// register_step_handler (registered here). Returns the padded reduction extent.
+int64_t pad_conv_channels(tir::Schedule& s, const std::string& block, int64_t multiple);
+
 // Full-geometry intrinsic name, e.g. "b200.c2d.n16_i1x56x56_c64_o64_k1x3x3_s1x1x1_p0x1x1_d1x1x1_g1".
 std::string conv_intrin_key(const tir_b200_conv_desc& d);
 
