@@ -21,6 +21,7 @@
 #include "../../include/tir_b200.h"
 #include "dep.cuh"
 #include "halo.cuh"
+#include "halo2.cuh"
 #include "igemm.cuh"
 #include "netops.cuh"
 #include "prep.cuh"
@@ -225,6 +226,28 @@ cudaError_t launch_pdl(void (*kernel)(Params), int grid, int block, size_t smem,
   attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, p);
+}
+
+// Same, as clusters of `cluster` CTAs along x (CTA pairs for cta_group::2 kernels).
+template <typename Params>
+cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, int block, size_t smem,
+                               cudaStream_t stream, const Params& p) {
+  static const bool no_pdl = getenv("TIR_B200_NO_PDL") != nullptr;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = no_pdl ? 0 : 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = cluster;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kernel, p);
 }
 
@@ -683,6 +706,29 @@ int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
   return TIR_B200_OK;
 }
 
+// The CTA-pair variant (halo2.cuh): 64 output channels, one group, TMA-store epilogue.
+int launch_halo2(tb::HaloParams& p, const uint16_t* W, cudaStream_t stream) {
+  const DeviceInfo di = device_info();
+  // weights: this CTA's 32-column half, boxes of b_box_rows rows (64-byte rows, SW64)
+  int rc = encode_2d(&p.tmW, W, p.b_rows, p.co, tb::kPairBHalf, p.b_box_rows);
+  if (rc) return rc;
+  const int fixed = 1024 + 256 + p.b_rows * tb::kPairBHalf * 2 + 2 * p.stage_bytes;
+  const int slab = p.slab_rows * 128;
+  const int stages = std::min(4, (di.smem_optin - fixed) / slab);
+  if (stages < 2) return kNotEligible;
+  p.stages = stages;
+  const size_t smem = tb::halo2_smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem)));
+  const int pairs = (p.total_tiles + 1) / 2;
+  int grid = 2 * std::min(pairs, di.sms / 2);
+  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(2, std::min(grid, atoi(e) / 2 * 2));
+  p.trace = g_trace;
+  CUDA_TRY(launch_pdl_cluster(tb::conv_halo2_kernel, grid, 2, tb::kHaloThreads, smem, stream, p));
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
 // Stride-1 2-D convolution as halo tiles (see halo.cuh). Returns kNotEligible
 // for shapes outside its envelope.
 int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
@@ -831,6 +877,12 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
     }
   }
   const bool k3 = KH == 3 && KW == 3;
+  // CTA pairs (halo2.cuh): M = 256 per MMA, half the weights per SM.
+  if (bn == 64 && g.co == 64 && g.g == 1 && p.tiles_n == 1 && !linear && (p.store_mode == 1 || p.store_mode == 2) &&
+      getenv("TIR_B200_PAIR")) {
+    const int rc = launch_halo2(p, W, stream);
+    if (rc != kNotEligible) return rc;
+  }
   // Tap-packed N (halo.cuh): 3x3 undilated, 64-column tiles, TMA-store epilogue.
   // Opt-in (TIR_B200_TAPN=1): measured on B200 it cuts the MMA time per C2D tile
   // from ~2500 to ~1150 cycles, but reading the 3x wider accumulator out of TMEM
