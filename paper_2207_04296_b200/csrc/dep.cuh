@@ -229,6 +229,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
   };
 
   if (threadIdx.x == 0) {
+    prefetch_tmap(&p.tmX);  // descriptor fetch overlaps the prologue
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_barrier_init();

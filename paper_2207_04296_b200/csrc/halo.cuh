@@ -110,6 +110,11 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 32 * 8 + 1) {  // descriptor fetches overlap the prologue
+    prefetch_tmap(&p.tmX);
+    prefetch_tmap(&p.tmW);
+    if (p.store_mode == 1 || p.store_mode == 2) prefetch_tmap(&p.tmY);
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], 1);

@@ -239,6 +239,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t lane = lane_id();
   constexpr uint32_t kMmaWarp = 8;
 
+  if (threadIdx.x == 32 * kMmaWarp + 1) {  // descriptor fetches overlap the prologue
+    for (int i = 0; i < p.num_sub; ++i) prefetch_tmap(&p.tmA[i]);
+    prefetch_tmap(&p.tmB);
+    if (p.store_mode) prefetch_tmap(&p.tmY);
+  }
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], kProducers);  // every producer arrives once per stage
