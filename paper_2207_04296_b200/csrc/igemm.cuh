@@ -41,8 +41,7 @@ namespace tb {
 
 constexpr int kBM = 128;
 constexpr int kBK = 64;  // K per sub-block (one 128-byte swizzle row of fp16)
-constexpr int kThreads = 288;
-constexpr int kProducers = 4;
+constexpr int kThreads = 288;  // 4 epilogue + 4 producer + 1 MMA warps (EPI8: 8 + 3 + 1 = 384)
 constexpr int kMaxPieces = 2048;  // per-launch piece table entries (16 B each)
 constexpr int kMaxSub = 4;
 
@@ -137,8 +136,17 @@ __device__ __forceinline__ int batch_col(const BatchAxis& a, int z1, int z2) {
   return a.col[0] + z1 * a.col[1] + z2 * a.col[2];
 }
 
-template <int BN, int KS>
+// EPI8: the short-K variant (1x1 convs / expansion GEMMs / attention, whose
+// tiles are a few MMAs and a 128 x BN epilogue): 8 epilogue warps — two per TMEM
+// lane quadrant, alternating column chunks — so two epilogue warps share each
+// SM sub-partition and overlap their latency-bound chunk chains; 3 producers
+// suffice for one or two stages per tile.
+template <int BN, int KS, bool EPI8 = false>
 struct IgemmCfg {
+  static constexpr int kEpiWarps = EPI8 ? 8 : 4;
+  static constexpr int kProd = EPI8 ? 3 : 4;
+  static constexpr int kMma = kEpiWarps + kProd;          // MMA warp (last)
+  static constexpr int kThreadsN = 32 * (kMma + 1);
   static constexpr int kSubA = kBM * kBK * 2;               // 16 KB per 64-deep sub-block
   static constexpr int kABytes = KS * kSubA;
   static constexpr int kBRows = KS * kBK;                   // B rows per stage
@@ -152,7 +160,7 @@ struct IgemmCfg {
   static constexpr uint32_t kIdesc = idesc_f16_f32(kBM, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
   // epilogue staging: per epilogue warp two 4 KB buffers (32 rows x 32 fp32)
   static constexpr int kEpiWarpBytes = 8192;
-  static constexpr int kEpiBytes = 4 * kEpiWarpBytes;
+  static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
   // smem: [A ring][B ring | resident panel][epilogue staging][piece table][barriers]
   static size_t smem_bytes(int stages, int b_res_rows, int pieces) {
     const size_t b = b_res_rows ? static_cast<size_t>(b_res_rows) * BN * 2
@@ -213,10 +221,12 @@ __device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& 
   return e;
 }
 
-template <int BN, int KS>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int BN, int KS, bool EPI8 = false>
+__global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     igemm_tc_kernel(const __grid_constant__ IgemmParams p) {
-  using Cfg = IgemmCfg<BN, KS>;
+  using Cfg = IgemmCfg<BN, KS, EPI8>;
+  constexpr int kProducers = Cfg::kProd;
+  constexpr int kEpi = Cfg::kEpiWarps;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -237,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  constexpr uint32_t kMmaWarp = 8;
+  constexpr uint32_t kMmaWarp = Cfg::kMma;
 
   if (threadIdx.x == 32 * kMmaWarp + 1) {  // descriptor fetches overlap the prologue
     for (int i = 0; i < p.num_sub; ++i) prefetch_tmap(&p.tmA[i]);
@@ -251,7 +261,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 128);
+      mbar_init(&tempty[i], 32 * kEpi);
     }
     mbar_init(bres_full, 1);
     fence_barrier_init();
@@ -264,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (p.a_mode != A_TILED) {
     for (int s = 0; s < p.num_sub; ++s) {
       const SubProb& sp = p.sub[s];
-      for (int pc = threadIdx.x; pc < sp.num_pieces; pc += kThreads)
+      for (int pc = threadIdx.x; pc < sp.num_pieces; pc += Cfg::kThreadsN)
         pieces[sp.piece_begin + pc] = make_piece(p, sp, pc);
     }
   }
@@ -279,7 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t t_start = 0;
   if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
-  if (warp >= 4 && warp < 4 + kProducers) {
+  if (warp >= kEpi && warp < kEpi + kProducers) {
     // ------------------------------------------------------------ producers
     pdl_wait();  // operands may be produced by the preceding kernel
     // Every producer walks every stage and issues a round-robin share of its
@@ -287,7 +297,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // stage's full barrier with its own expect_tx. A single issuing thread
     // completes about one request per ~500 cycles (tools/tmabw.cu), so a stage's
     // requests are spread over four issuers.
-    const int pw = static_cast<int>(warp) - 4;
+    const int pw = static_cast<int>(warp) - kEpi;
     const int box = p.a_box_ch;
     const int pps = KS * (kBK / box);  // pieces per stage
     const uint32_t piece_bytes = kBM * box * 2;
@@ -476,11 +486,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         acc_phase ^= 1;
       }
     }
-  } else if (warp < 4) {
+  } else if (warp < kEpi) {
     // ------------------------------------------------------------ epilogue
     pdl_wait();  // Y / Yin may be in use by the preceding kernel
-    const uint32_t q = warp & 3;
-    uint8_t* wbuf = epi_smem + q * Cfg::kEpiWarpBytes;
+    const uint32_t q = warp & 3, hh = warp >> 2;
+    constexpr int kHs = kEpi / 4;  // column chunks are dealt round-robin over the kHs warps of a quadrant
+    uint8_t* wbuf = epi_smem + warp * Cfg::kEpiWarpBytes;
     uint32_t acc = 0, acc_phase = 0, chunk = 0;
     if (p.store_mode) {
       // TMA store: thread = tile row (tcgen05.ld 32x32b); each warp stages its
@@ -511,7 +522,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int64_t col_tile = colb_tile + c_c;                               // column of the C tensor
         const int valid_tile = p.cog - nt * BN;  // columns of this tile inside the group
         // bias of the next 32 columns, one column per lane (prefetched a chunk ahead)
-        float bnext = (p.bias && static_cast<int>(lane) < valid_tile) ? __ldg(p.bias + colb_tile + lane) : 0.0f;
+        const int c_first = static_cast<int>(hh) * cw;  // this warp's first chunk
+        float bnext = (p.bias && c_first + static_cast<int>(lane) < valid_tile)
+                          ? __ldg(p.bias + colb_tile + c_first + lane) : 0.0f;
         // residual rows past M are clipped by the TMA store and never read
         const uint16_t* res_row = (p.residual && row_local < p.sub[0].m_count)
                                       ? p.residual + row * p.ldy + col_tile : nullptr;
@@ -522,12 +535,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = 0; i < 4; ++i) rp[i] = __ldg(reinterpret_cast<const uint4*>(res_row + c) + i);
           }
         };
-        fetch_res(0);
+        fetch_res(c_first);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += cw, ++chunk) {
+        for (int c0 = c_first; c0 < BN; c0 += kHs * cw, ++chunk) {
           if (c0 >= valid_tile) continue;  // warp-uniform: chunk past the group
           uint8_t* buf = wbuf + (chunk & 1) * 4096;
           uint8_t* dst = buf + lane * line_bytes;
@@ -536,6 +549,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           for (int h = 0; h < cw; h += 32) {
             uint32_t r[32];
             const int cc = c0 + h;
+            const int next_cc = h + 32 < cw ? cc + 32 : c0 + kHs * cw;  // this warp's next 32 columns
             tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + cc, r);
             tmem_ld_wait();
             const int lim = valid_tile - cc;
@@ -545,7 +559,7 @@ __global__ void __launch_bounds__(kThreads, 1)
               // C-ABI order: + bias, + residual, activation
               if (p.bias) {
                 const float bcur = bnext;
-                const int nc = cc + 32 + static_cast<int>(lane);
+                const int nc = next_cc + static_cast<int>(lane);
                 bnext = nc < valid_tile ? __ldg(p.bias + colb_tile + nc) : 0.0f;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bcur, i);
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                       v[i] += __half2float(__ushort_as_half(
                           __ldg(reinterpret_cast<const unsigned short*>(res_row + cc) + i)));
                 }
-                fetch_res(cc + 32);  // in flight during this chunk's conversion and store
+                fetch_res(next_cc);  // in flight during this chunk's conversion and store
               }
               epi_act_n<32>(v, p.relu);
             }
@@ -657,7 +671,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kLanesPerRow = kChunk / 4;
         constexpr int kRowsPerPass = 32 / kLanesPerRow;
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += kChunk) {
+        for (int c0 = static_cast<int>(hh) * kChunk; c0 < BN; c0 += kHs * kChunk) {
           uint32_t r[32];
           const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN + c0;
           if (kChunk == 32) tmem_ld_32x32b_x32(taddr, r);
