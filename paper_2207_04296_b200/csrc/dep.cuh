@@ -253,13 +253,17 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
     const int slot = k & 1;
     int n, oy0, ox0, c0;
     tile_coords(t, n, oy0, ox0, c0);
+    // channel vector of this thread inside C? (C % 32 != 0, e.g. MobileNet-V2's 144:
+    // the last 32-channel block is partial; TMA zero-fills its input channels >= C)
+    const bool cv_ok = c0 + cv * 8 < p.c;
     if (c0 != cur_c0) {  // weights -> registers (once per channel block)
       cur_c0 = c0;
 #pragma unroll
       for (int rh = 0; rh < K; ++rh)
 #pragma unroll
         for (int rw = 0; rw < K; ++rw) {
-          const uint4 u = __ldg(reinterpret_cast<const uint4*>(p.W + (rh * K + rw) * p.c + c0 + cv * 8));
+          const uint4 u = cv_ok ? __ldg(reinterpret_cast<const uint4*>(p.W + (rh * K + rw) * p.c + c0 + cv * 8))
+                                : make_uint4(0, 0, 0, 0);
           const __half2* h = reinterpret_cast<const __half2*>(&u);
 #pragma unroll
           for (int v = 0; v < 4; ++v) w[rh][rw][v] = pack_f32x2(__half22float2(h[v]));
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
 #pragma unroll
       for (int tt = 0; tt < T; ++tt) {
         const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + tt;
-        if (p.accumulate && oy < p.oh && ox < p.ow) {
+        if (p.accumulate && cv_ok && oy < p.oh && ox < p.ow) {
           const float* yin = p.Yin + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
           const float4 a = *reinterpret_cast<const float4*>(yin);
           const float4 bb = *reinterpret_cast<const float4*>(yin + 4);
@@ -320,7 +324,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
 #pragma unroll
       for (int tt = 0; tt < T; ++tt) {
         const int oy = oy0 + tr * R + r, ox = ox0 + tc * T + tt;
-        if (oy >= p.oh || ox >= p.ow) continue;
+        if (oy >= p.oh || ox >= p.ow || !cv_ok) continue;
         const int64_t off = ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.c + c0 + cv * 8;
         float2 f[4];
 #pragma unroll

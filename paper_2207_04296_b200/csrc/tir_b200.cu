@@ -1192,7 +1192,7 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   p.pad_w = static_cast<int32_t>(g.p[2]);
   p.tiles_h = static_cast<int32_t>((g.out[1] + TR - 1) / TR);
   p.tiles_w = static_cast<int32_t>((g.out[2] + TC - 1) / TC);
-  p.cblocks = static_cast<int32_t>(g.ci / 32);
+  p.cblocks = static_cast<int32_t>((g.ci + 31) / 32);  // a partial last block when C % 32 != 0
   p.accumulate = accumulate;
   p.bias = epi.bias;
   p.relu = epi.relu;
@@ -1222,7 +1222,7 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
   const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0) &&
                        (!accumulate || reinterpret_cast<uintptr_t>(Yin) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-  if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 32 == 0 && g.k[1] == 3 && g.k[2] == 3 &&
+  if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 8 == 0 && g.ci >= 32 && g.k[1] == 3 && g.k[2] == 3 &&
       g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
     const int64_t ow = g.out[2];
     const char* tc_env = getenv("TIR_B200_DEP_TC");  // tile-shape override (tuning)

@@ -72,6 +72,10 @@ SMALL = {
     "DEP_7": tb.Conv("DEP", n=5, in_dhw=(1, 7, 7), ci=96, co=96, k=(1, 3, 3), p=(0, 1, 1), groups=96),
     "DEP_s2_14": tb.Conv("DEP", n=3, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
                          groups=64),
+    # C % 32 != 0: partial last channel block in the TMA tile kernel (MobileNet-V2 144 / 24 channels)
+    "DEP_c144": tb.Conv("DEP", n=2, in_dhw=(1, 20, 20), ci=144, co=144, k=(1, 3, 3), p=(0, 1, 1), groups=144),
+    "DEP_c40_s2": tb.Conv("DEP", n=2, in_dhw=(1, 17, 17), ci=40, co=40, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
+                          groups=40),
     "DEP_c12": tb.Conv("DEP", n=1, in_dhw=(1, 7, 7), ci=12, co=12, k=(1, 5, 5), p=(0, 2, 2), groups=12),
 }
 
