@@ -190,6 +190,99 @@ inline int launch_pack_kw_fused(const uint16_t* x, uint16_t* y, const uint16_t* 
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
+// (kh, kw, c) packing for CI = 3 stems whose KH*KW*CI exceeds 64 (C3D's and
+// DIL's 7x7 windows, 147 values): Xp[n, d, oh, ow, j] = X[n, d, oh*sh - ph + kh*dh,
+// ow*sw - pw + kw*dw, c] with j = (kh*KW + kw)*C + c (zero where out of bounds or
+// j >= KH*KW*C), cp a multiple of 64 so the conv that remains (depth taps only)
+// streams 64-channel im2col pieces instead of request-bound 32-channel ones.
+// Block = one output row (n, d, oh): the KH input rows it needs (KH * W * C
+// halves) are staged in shared memory; threads emit 16-byte output vectors from
+// a (kh, kw, c) table. The weights [KD][KH][KW][C][CO] are already in j order
+// per kd: Wp[kd][j][co] is a copy with zero rows j >= KH*KW*C (extra blocks).
+__global__ void __launch_bounds__(256) pack_hw_kernel(
+    const uint16_t* __restrict__ x, uint16_t* __restrict__ y, const uint16_t* __restrict__ w,
+    uint16_t* __restrict__ wy, int32_t rows, int32_t ih, int32_t iw, int32_t c, int32_t oh, int32_t ow,
+    int32_t kh, int32_t kw, int32_t sh, int32_t sw, int32_t ph, int32_t pw, int32_t dh, int32_t dw, int32_t cp,
+    int32_t kd, int32_t co) {
+  extern __shared__ __align__(16) uint16_t srows[];  // [kh][iw * c]
+  __shared__ int16_t tab_h[256], tab_w[256], tab_c[256];
+  const int32_t taps_c = kh * kw * c;
+  if (static_cast<int32_t>(blockIdx.x) >= rows) {  // weights
+    const int64_t total = static_cast<int64_t>(kd) * cp * co;
+    const int64_t step = static_cast<int64_t>(gridDim.x - rows) * blockDim.x;
+    for (int64_t i = (blockIdx.x - rows) * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total; i += step) {
+      const int32_t col = static_cast<int32_t>(i % co);
+      const int64_t r = i / co;
+      const int32_t g = static_cast<int32_t>(r / cp), j = static_cast<int32_t>(r % cp);
+      wy[i] = j < taps_c ? w[(static_cast<int64_t>(g) * taps_c + j) * co + col] : static_cast<uint16_t>(0);
+    }
+    return;
+  }
+  for (int j = threadIdx.x; j < cp; j += blockDim.x) {
+    const int t = j / c;
+    tab_h[j] = static_cast<int16_t>(j < taps_c ? t / kw : -1);
+    tab_w[j] = static_cast<int16_t>(t % kw);
+    tab_c[j] = static_cast<int16_t>(j % c);
+  }
+  // row = (n*D + d)*OH + oy
+  const int32_t oy = static_cast<int32_t>(blockIdx.x) % oh;
+  const int64_t nd = static_cast<int64_t>(blockIdx.x) / oh;
+  const int32_t row_elems = iw * c;
+  for (int t = 0; t < kh; ++t) {
+    const int32_t y_in = oy * sh - ph + t * dh;
+    uint16_t* dst = srows + t * row_elems;
+    if (y_in < 0 || y_in >= ih) {
+      for (int v = threadIdx.x; v < row_elems; v += blockDim.x) dst[v] = 0;
+    } else {
+      const uint16_t* src = x + (nd * ih + y_in) * row_elems;
+      for (int v = threadIdx.x; v < row_elems; v += blockDim.x) dst[v] = __ldg(src + v);
+    }
+  }
+  __syncthreads();
+  const int32_t nvec = ow * (cp / 8);
+  uint4* yr = reinterpret_cast<uint4*>(y + static_cast<int64_t>(blockIdx.x) * ow * cp);
+  for (int32_t v = threadIdx.x; v < nvec; v += blockDim.x) {
+    const int32_t o = v / (cp / 8), grp = v - o * (cp / 8);
+    const int32_t base = o * sw - pw;
+    uint16_t e8[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const int32_t j = grp * 8 + e;
+      const int32_t th = tab_h[j];
+      const int32_t wi = base + tab_w[j] * dw;
+      e8[e] = (th >= 0 && wi >= 0 && wi < iw) ? srows[th * row_elems + wi * c + tab_c[j]] : static_cast<uint16_t>(0);
+    }
+    uint4 u;
+    u.x = e8[0] | (static_cast<uint32_t>(e8[1]) << 16);
+    u.y = e8[2] | (static_cast<uint32_t>(e8[3]) << 16);
+    u.z = e8[4] | (static_cast<uint32_t>(e8[5]) << 16);
+    u.w = e8[6] | (static_cast<uint32_t>(e8[7]) << 16);
+    yr[v] = u;
+  }
+}
+
+inline int launch_pack_hw(const uint16_t* x, uint16_t* y, const uint16_t* w, uint16_t* wy, int64_t rows, int64_t ih,
+                          int64_t iw, int64_t c, int64_t oh, int64_t ow, int64_t kh, int64_t kw, int64_t sh,
+                          int64_t sw, int64_t ph, int64_t pw, int64_t dh, int64_t dw, int64_t cp, int64_t kd,
+                          int64_t co, cudaStream_t st) {
+  const size_t smem = static_cast<size_t>(kh * iw * c * 2);
+  if (smem > 96 * 1024 || rows >= (1ll << 31) - 64 || cp > 256) return 2;  // caller falls back
+  static bool attr_set = false;
+  if (!attr_set) {
+    if (cudaFuncSetAttribute(pack_hw_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024) != cudaSuccess)
+      return 1;
+    attr_set = true;
+  }
+  const int wblocks = 16;
+  pack_hw_kernel<<<static_cast<unsigned>(rows + wblocks), 256, smem, st>>>(
+      x, y, w, wy, static_cast<int32_t>(rows), static_cast<int32_t>(ih), static_cast<int32_t>(iw),
+      static_cast<int32_t>(c), static_cast<int32_t>(oh), static_cast<int32_t>(ow), static_cast<int32_t>(kh),
+      static_cast<int32_t>(kw), static_cast<int32_t>(sh), static_cast<int32_t>(sw), static_cast<int32_t>(ph),
+      static_cast<int32_t>(pw), static_cast<int32_t>(dh), static_cast<int32_t>(dw), static_cast<int32_t>(cp),
+      static_cast<int32_t>(kd), static_cast<int32_t>(co));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 inline int grid_for(int64_t n) {
   int64_t b = (n + 255) / 256;
   return static_cast<int>(b < 1 ? 1 : (b > 148 * 32 ? 148 * 32 : b));

@@ -923,6 +923,45 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   int64_t cig = g.ci / g.g;
   const int64_t cog = g.co / g.g;
   int64_t taps = g.k[0] * g.k[1] * g.k[2];
+  // Small-channel layers whose KH x KW window is large (C3D / DIL 7x7 x CI=3 =
+  // 147 values): pack (kh, kw, c) into 64-aligned channels (pack_hw, prep.cuh);
+  // what remains is a depth-only (C3D) or 1x1 (DIL) conv streaming 64-channel
+  // im2col pieces. Bit-exact relayout. Opt-in (TIR_B200_PACK_HW=1): measured on
+  // B200 the 6.4x larger relayout (1.23 GB for the C3D paper shape, written and
+  // read back through HBM) costs more than the request-bound 32-channel pieces
+  // it removes (C3D 1260 vs 724 us).
+  if (cig % 8 && g.g == 1 && !g.transposed && g.k[1] * g.k[2] * cig > 64 && g.k[1] * g.k[2] * cig <= 256 &&
+      getenv("TIR_B200_PACK_HW")) {
+    const int64_t khwc = g.k[1] * g.k[2] * cig;
+    const int64_t cp = (khwc + 63) / 64 * 64;
+    const int64_t rows = g.n * g.in[0] * g.out[1];
+    const size_t xbytes = static_cast<size_t>(rows * g.out[2] * cp * 2);
+    const size_t wbytes = static_cast<size_t>(g.k[0] * cp * g.co * 2);
+    void* ws = nullptr;
+    int rc = workspace(xbytes + wbytes + 512, &ws);
+    if (rc) return rc;
+    uint16_t* Xp = static_cast<uint16_t*>(ws);
+    uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
+    const int prc = tb::launch_pack_hw(X, Xp, W, Wp, rows, g.in[1], g.in[2], cig, g.out[1], g.out[2], g.k[1], g.k[2],
+                                       g.s[1], g.s[2], g.p[1], g.p[2], g.d[1], g.d[2], cp, g.k[0], g.co, stream);
+    if (prc == 1) return set_err(TIR_B200_ERR_CUDA, "pack kernel launch failed");
+    if (prc == 0) {
+      ++g_launches;
+      X = Xp;
+      W = Wp;
+      g.in[1] = g.out[1];
+      g.in[2] = g.out[2];
+      g.ci = cp;
+      for (int i = 1; i < 3; ++i) {
+        g.k[i] = 1;
+        g.s[i] = 1;
+        g.p[i] = 0;
+        g.d[i] = 1;
+      }
+      cig = cp;
+      taps = g.k[0];
+    }
+  }
   // Small-channel layers (CI = 3 in C3D / DIL): pack the KW taps into the
   // channel dim ((kw, c) packing, prep.cuh) so each im2col piece carries
   // KW*CI real channels instead of CI padded to 8. Bit-exact relayout.

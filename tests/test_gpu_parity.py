@@ -280,3 +280,14 @@ def test_opt_in_halo_variants_exact(variant, monkeypatch, cuda):
             assert O.tensors_bitwise_equal(got[img:img + 1], want), (variant, img)
             ref16 = np.maximum(want + bias, 0).astype(np.float16).astype(np.float32)
             assert np.array_equal(fused[img:img + 1], ref16), (variant, img)
+
+
+@pytest.mark.parametrize("name", ["DIL", "C3D"])
+def test_opt_in_pack_hw_exact(name, monkeypatch, cuda):
+    """The opt-in (kh, kw, c) relayout (TIR_B200_PACK_HW) stays bit-exact."""
+    monkeypatch.setenv("TIR_B200_PACK_HW", "1")
+    spec = SMALL[name]
+    x = O.reference_tensor(spec.x_shape(), 31)
+    w = O.reference_tensor(spec.w_shape(), 32)
+    got = run_conv(spec, x, w, cuda)
+    assert O.tensors_bitwise_equal(got, O.conv(ospec(spec), x, w, threads=8))
