@@ -1339,6 +1339,8 @@ int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t*
 struct HostCache {
   int dev = -1;
   cudaStream_t stream = nullptr;
+  cudaStream_t side[2] = {nullptr, nullptr};  // batch-chunk pipeline streams
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   void* dbuf = nullptr;
   size_t dbytes = 0;
   int* dflag = nullptr;
@@ -1351,6 +1353,8 @@ int host_prepare(size_t bytes, char** base) {
   if (t_host.dev != dev) {
     tir_b200_release_host_cache();
     CUDA_TRY(cudaStreamCreateWithFlags(&t_host.stream, cudaStreamNonBlocking));
+    for (auto& st : t_host.side) CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    for (auto& e : t_host.ev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(&t_host.dflag), sizeof(int)));
     t_host.dev = dev;
   }
@@ -1452,13 +1456,36 @@ int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const 
   rc = host_prepare(xa + wa + ya, &d);
   if (rc) return rc;
   cudaStream_t st = t_host.stream;
-  CUDA_TRY(cudaMemcpyAsync(d, X, xe * 2, cudaMemcpyHostToDevice, st));
   CUDA_TRY(cudaMemcpyAsync(d + xa, W, we * 2, cudaMemcpyHostToDevice, st));
-  if (accumulate) CUDA_TRY(cudaMemcpyAsync(d + xa + wa, Y, ye * 4, cudaMemcpyHostToDevice, st));
-  rc = conv_impl(desc, reinterpret_cast<uint16_t*>(d), reinterpret_cast<uint16_t*>(d + xa),
-                 reinterpret_cast<float*>(d + xa + wa), d + xa + wa, accumulate, 0, Epi{}, st);
-  if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(Y, d + xa + wa, ye * 4, cudaMemcpyDeviceToHost, st));
+  // Batch-chunk pipeline: images are independent (every output keeps its own
+  // reduction order, so a batch slice is bit-identical), so chunk c's H2D, conv
+  // and D2H are queued on one of three streams and the two PCIe directions and
+  // the GPU overlap across chunks. Only for convs that need no shared library
+  // workspace (CI / G a multiple of 8: no relayout kernels).
+  const int64_t cig = g.ci / g.g;
+  const int nch = (cig % 8 == 0 && g.n >= 2 && !getenv("TIR_B200_NO_HOST_PIPELINE"))
+                      ? static_cast<int>(std::min<int64_t>(g.n, 8)) : 1;
+  const int64_t x_img = xe / g.n, y_img = ye / g.n;
+  CUDA_TRY(cudaEventRecord(t_host.ev[0], st));  // weights uploaded
+  cudaStream_t streams[3] = {st, t_host.side[0], t_host.side[1]};
+  for (int c = 1; c < 3 && c < nch; ++c) CUDA_TRY(cudaStreamWaitEvent(streams[c], t_host.ev[0], 0));
+  for (int c = 0; c < nch; ++c) {
+    const int64_t n0 = g.n * c / nch, n1 = g.n * (c + 1) / nch;
+    cudaStream_t sc = streams[c % 3];
+    uint16_t* dx = reinterpret_cast<uint16_t*>(d) + n0 * x_img;
+    float* dy = reinterpret_cast<float*>(d + xa + wa) + n0 * y_img;
+    CUDA_TRY(cudaMemcpyAsync(dx, X + n0 * x_img, (n1 - n0) * x_img * 2, cudaMemcpyHostToDevice, sc));
+    if (accumulate) CUDA_TRY(cudaMemcpyAsync(dy, Y + n0 * y_img, (n1 - n0) * y_img * 4, cudaMemcpyHostToDevice, sc));
+    tir_b200_conv_desc dc = *desc;
+    dc.n = n1 - n0;
+    rc = conv_impl(&dc, dx, reinterpret_cast<uint16_t*>(d + xa), dy, dy, accumulate, 0, Epi{}, sc);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(Y + n0 * y_img, dy, (n1 - n0) * y_img * 4, cudaMemcpyDeviceToHost, sc));
+  }
+  for (int c = 1; c < 3 && c < nch; ++c) {
+    CUDA_TRY(cudaEventRecord(t_host.ev[c], streams[c]));
+    CUDA_TRY(cudaStreamWaitEvent(st, t_host.ev[c], 0));
+  }
   CUDA_TRY(cudaStreamSynchronize(st));
   return TIR_B200_OK;
 }
@@ -1660,6 +1687,10 @@ void tir_b200_release_host_cache(void) {
     if (t_host.dbuf) cudaFree(t_host.dbuf);
     if (t_host.dflag) cudaFree(t_host.dflag);
     if (t_host.stream) cudaStreamDestroy(t_host.stream);
+    for (auto st : t_host.side)
+      if (st) cudaStreamDestroy(st);
+    for (auto e : t_host.ev)
+      if (e) cudaEventDestroy(e);
     cudaSetDevice(cur);
   }
   t_host = HostCache{};

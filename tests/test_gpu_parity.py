@@ -291,3 +291,17 @@ def test_opt_in_pack_hw_exact(name, monkeypatch, cuda):
     w = O.reference_tensor(spec.w_shape(), 32)
     got = run_conv(spec, x, w, cuda)
     assert O.tensors_bitwise_equal(got, O.conv(ospec(spec), x, w, threads=8))
+
+
+def test_host_path_batch_pipeline_exact(cuda):
+    """tir_b200_conv_host splits the batch into chunks pipelined over three
+    streams (H2D / conv / D2H overlap): uneven chunks, accumulate, bit-exact."""
+    spec = tb.Conv("C2D", n=5, in_dhw=(1, 9, 11), ci=64, co=64, k=(1, 3, 3), p=(0, 1, 1))
+    x = O.reference_tensor(spec.x_shape(), 41)
+    w = O.reference_tensor(spec.w_shape(), 42)
+    y0 = O.reference_tensor(spec.y_shape(), 43)
+    want = O.conv(ospec(spec), x, w, threads=8)
+    got = tb.conv_host(spec, x.astype(np.float16), w.astype(np.float16))
+    assert O.tensors_bitwise_equal(got, want)
+    acc = tb.conv_host(spec, x.astype(np.float16), w.astype(np.float16), y0.copy(), accumulate=True)
+    assert O.tensors_bitwise_equal(acc, O.conv(ospec(spec), x, w, y0, threads=8))
