@@ -326,7 +326,10 @@ __device__ __forceinline__ float gelu_erf(float v) {
 // max(x, 0.0) (std::max: (v < 0) ? 0 : v, so NaN and -0.0 pass through).
 __device__ __forceinline__ float epi_act(float v, int act) {
   if (act == 1) return (v < 0.0f) ? 0.0f : v;
-  if (act == 2) return (v < 0.0f) ? 0.0f : (v > 6.0f ? 6.0f : v);
+  if (act == 2) {
+    v = (v < 0.0f) ? 0.0f : v;  // two flat selects: the nested ternary compiled
+    return (v > 6.0f) ? 6.0f : v;  // to a divergent branch per element
+  }
   if (act == 3) return gelu_erf(v);
   return v;
 }
@@ -340,7 +343,10 @@ __device__ __forceinline__ void epi_act_n(float* v, int act) {
     for (int i = 0; i < N; ++i) v[i] = (v[i] < 0.0f) ? 0.0f : v[i];
   } else if (act == 2) {
 #pragma unroll
-    for (int i = 0; i < N; ++i) v[i] = (v[i] < 0.0f) ? 0.0f : (v[i] > 6.0f ? 6.0f : v[i]);
+    for (int i = 0; i < N; ++i) {
+      const float a = (v[i] < 0.0f) ? 0.0f : v[i];
+      v[i] = (a > 6.0f) ? 6.0f : a;
+    }
   } else if (act == 3) {
 #pragma unroll
     for (int i = 0; i < N; ++i) v[i] = gelu_erf(v[i]);

@@ -75,3 +75,4 @@ for K, N in KN:
     show(f"M{M} K{K} N{N} f16 relu", lambda: tb.gmm(A, B, C16, out_f16=True, relu=True))
     show(f"M{M} K{K} N{N} f16 bias+relu", lambda: tb.gmm(A, B, C16, out_f16=True, bias=bias, relu=True))
     show(f"M{M} K{K} N{N} f16 bias+res+relu", lambda: tb.gmm(A, B, C16, out_f16=True, bias=bias, relu=True, residual=R))
+    show(f"M{M} K{K} N{N} f16 bias+relu6", lambda: tb.gmm(A, B, C16, out_f16=True, bias=bias, relu="relu6"))
