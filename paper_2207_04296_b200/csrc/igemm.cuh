@@ -109,6 +109,7 @@ struct alignas(64) IgemmParams {
   const float* Yin;
   int32_t store_mode;  // 0: generic row-offset stores, 1: TMA store, 2: TMA reduce-add (Y += tile)
   int32_t epi_cw;      // store modes 1/2: columns per staged chunk (32, or 64 for fp16 with BN >= 64)
+  int32_t bias_floats; // > 0: the whole bias vector is staged in shared memory (16-byte broadcasts)
   int32_t ksplit;      // split-K partitions (>= 1); > 1 adds partials into a pre-initialised Y
   int32_t reduce;      // generic path: red.global.add into Y instead of stores (split-K)
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
@@ -162,11 +163,11 @@ struct IgemmCfg {
   static constexpr int kEpiWarpBytes = 8192;
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
   // smem: [A ring][B ring | resident panel][epilogue staging][piece table][barriers]
-  static size_t smem_bytes(int stages, int b_res_rows, int pieces) {
+  static size_t smem_bytes(int stages, int b_res_rows, int pieces, int bias_floats) {
     const size_t b = b_res_rows ? static_cast<size_t>(b_res_rows) * BN * 2
                                 : static_cast<size_t>(stages) * kBBytes;
     return 1024 /*align slack*/ + static_cast<size_t>(stages) * kABytes + b + kEpiBytes +
-           static_cast<size_t>(pieces) * sizeof(int4) + 256 /*barriers*/;
+           static_cast<size_t>(pieces) * sizeof(int4) + static_cast<size_t>(bias_floats) * 4 + 256 /*barriers*/;
   }
 };
 
@@ -238,7 +239,9 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
                                : static_cast<size_t>(S) * Cfg::kBBytes;
   uint8_t* epi_smem = sB0 + b_bytes;  // 1024-aligned (all preceding sizes are)
   int4* pieces = reinterpret_cast<int4*>(epi_smem + Cfg::kEpiBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(pieces + p.total_pieces);
+  // staged fp32 bias (p.bias_floats columns; 0 = read from global with shuffles)
+  float* sbias = reinterpret_cast<float*>(pieces + p.total_pieces);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbias + p.bias_floats);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;            // [kNacc]
   uint64_t* tempty = tfull + Cfg::kNacc;  // [kNacc]
@@ -269,6 +272,10 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   if (warp == kMmaWarp) {
     tmem_alloc(tmem_slot, Cfg::kTmemCols);
     tmem_relinquish();
+  }
+  if (p.bias_floats) {
+    pdl_wait();  // the bias may be produced by the preceding kernel
+    for (int i = threadIdx.x; i < p.bias_floats; i += Cfg::kThreadsN) sbias[i] = __ldg(p.bias + i);
   }
   // Piece table (all threads).
   if (p.a_mode != A_TILED) {
@@ -557,7 +564,15 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
             if (epi_on) {
               float* v = reinterpret_cast<float*>(r);
               // C-ABI order: + bias, + residual, activation
-              if (p.bias) {
+              if (p.bias && p.bias_floats && lim >= 32) {
+                // staged bias: eight 16-byte shared-memory broadcasts per 32 columns
+                const float4* b4 = reinterpret_cast<const float4*>(sbias + colb_tile + cc);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  const float4 b = b4[i];
+                  v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+                }
+              } else if (p.bias) {
                 const float bcur = bnext;
                 const int nc = next_cc + static_cast<int>(lane);
                 bnext = nc < valid_tile ? __ldg(p.bias + colb_tile + nc) : 0.0f;

@@ -258,7 +258,17 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   using Cfg = tb::IgemmCfg<BN, KS, EPI8>;
   const DeviceInfo di = device_info();
   const int table = p.total_pieces * 16;
-  const int budget = di.smem_optin - 1024 - 256 - table - Cfg::kEpiBytes;
+  // Stage the bias in shared memory for the TMA-store epilogue when it is small
+  // and every 32-column chunk starts 16-byte aligned inside it.
+  // Only for short-K (epilogue-bound) tiles: K-heavy GEMMs need the shared memory for pipeline stages.
+  int nst_all = 0;
+  for (int i = 0; i < p.num_sub; ++i) nst_all = std::max(nst_all, p.sub[i].num_stages);
+  const int nbias = p.groups * p.cog;
+  p.bias_floats = (p.bias && p.store_mode && !p.batch_tiles && nst_all * KS * tb::kBK <= 256 && nbias <= 4096 &&
+                   p.cog % 32 == 0 &&
+                   (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0 && !getenv("TIR_B200_NO_SMEM_BIAS"))
+                      ? (nbias + 3) / 4 * 4 : 0;
+  const int budget = di.smem_optin - 1024 - 256 - table - p.bias_floats * 4 - Cfg::kEpiBytes;
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
   const int keys = p.groups * p.tiles_n * p.ksplit;  // CTAs per B-panel cycle
@@ -278,7 +288,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes));
   }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
-  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces);
+  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces, p.bias_floats);
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
