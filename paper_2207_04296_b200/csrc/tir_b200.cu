@@ -940,10 +940,15 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   // B200 the 6.4x larger relayout (1.23 GB for the C3D paper shape, written and
   // read back through HBM) costs more than the request-bound 32-channel pieces
   // it removes (C3D 1260 vs 724 us).
-  if (cig % 8 && g.g == 1 && !g.transposed && g.k[1] * g.k[2] * cig > 64 && g.k[1] * g.k[2] * cig <= 256 &&
-      getenv("TIR_B200_PACK_HW")) {
-    const int64_t khwc = g.k[1] * g.k[2] * cig;
-    const int64_t cp = (khwc + 63) / 64 * 64;
+  // Default when the (kh, kw, c) relayout is no bigger than 1.5x the (kw, c) one
+  // (e.g. MobileNet-V2's 3x3 stem: 27 -> 32 channels, the same bytes as the
+  // (kw, c) form, and the conv becomes a 1x1 GEMM instead of 16-channel pieces).
+  const int64_t hw_cp = (g.k[1] * g.k[2] * cig + 63) / 64 * 64 <= 32 ? 32 : (g.k[1] * g.k[2] * cig + 63) / 64 * 64;
+  const int64_t kw_cp = g.k[2] * cig <= 8 ? 8 : g.k[2] * cig <= 16 ? 16 : g.k[2] * cig <= 32 ? 32 : 64;
+  const bool hw_small = g.out[1] * hw_cp * 2 <= 3 * g.in[1] * kw_cp;  // per output column, per image row block
+  if (cig % 8 && g.g == 1 && !g.transposed && g.k[1] > 1 && g.k[1] * g.k[2] * cig <= 256 &&
+      (getenv("TIR_B200_PACK_HW") || (hw_small && !getenv("TIR_B200_NO_PACK_HW")))) {
+    const int64_t cp = hw_cp;
     const int64_t rows = g.n * g.in[0] * g.out[1];
     const size_t xbytes = static_cast<size_t>(rows * g.out[2] * cp * 2);
     const size_t wbytes = static_cast<size_t>(g.k[0] * cp * g.co * 2);
