@@ -205,7 +205,15 @@ def test_gmm_d2_and_variants(mnk, cuda):
     assert O.tensors_close_dot(c.cpu().numpy(), want, abs_sum, REL_TOL_D2, DOT_TOL_D2)
     assert O.tensors_close_dot(C.cpu().numpy(), O.gmm(a, b, c0, threads=8), abs_sum + np.abs(c0),
                                REL_TOL_D2, DOT_TOL_D2)
-    assert np.array_equal(ch.cpu().numpy(), c.cpu().numpy().astype(np.float16))
+    # fp16 output = RN of an fp32 sum; the fp32-output launch may split K (a
+    # different fp32 summation order), so on N(0,1) data the two agree to one fp16 ulp
+    c32 = c.cpu().numpy()
+    c16 = c32.astype(np.float16)
+    got16 = ch.cpu().numpy()
+    ulp = np.spacing(np.abs(c16)).astype(np.float32)
+    # one fp16 ulp, plus the reassociation bound of the two fp32 sums where the result cancels
+    assert (np.abs(got16.astype(np.float32) - c16.astype(np.float32)) <= ulp + 2 * DOT_TOL_D2 * abs_sum).all()
+    assert np.mean(got16 == c16) > 0.99
 
 
 def test_gmm_unsupported_and_value_errors(cuda):
