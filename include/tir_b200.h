@@ -176,6 +176,8 @@ typedef struct {
   int64_t a_row[3], a_col[3]; /* base, per-z1 step, per-z2 step */
   int64_t b_row[3], b_col[3];
   int64_t c_row[3], c_col[3];
+  int64_t b_kmajor; /* 1: B is given transposed, B_z[k, n] = B[br + n, bc + k] (K contiguous,
+                       e.g. attention's K rows read straight from the QKV tensor) */
 } tir_b200_batch_desc;
 
 int tir_b200_gmm_batched(const uint16_t* A, int64_t a_rows, int64_t lda, const uint16_t* B,

@@ -101,7 +101,7 @@ class Conv:
 class BatchDesc(ctypes.Structure):
     """tir_b200_batch_desc: per-problem coordinates base + z1*step1 + z2*step2."""
     _fields_ = [("z1n", ctypes.c_int64), ("z2n", ctypes.c_int64)] + [
-        (f"{t}_{d}", ctypes.c_int64 * 3) for t in "abc" for d in ("row", "col")]
+        (f"{t}_{d}", ctypes.c_int64 * 3) for t in "abc" for d in ("row", "col")] + [("b_kmajor", ctypes.c_int64)]
 
 
 class Epilogue(ctypes.Structure):
@@ -333,10 +333,12 @@ def transpose(X, col0: int, cols: int, Y=None, *, stream=None):
 
 
 def gmm_batched(A, B, C, M: int, N: int, K: int, z: tuple, a: tuple, b: tuple, c: tuple, *,
-                out_f16: bool = True, bias=None, relu=False, residual=None, stream=None):
+                b_kmajor: bool = False, out_f16: bool = True, bias=None, relu=False, residual=None,
+                stream=None):
     """Batched GMM over strided windows of 2-D tensors (include/tir_b200.h):
-    problem (z1, z2) computes C[cr + m, cc + n] = sum_k A[ar + m, ac + k] * B[br + k, bc + n],
-    each coordinate given as ((base, step1, step2) for rows, (base, step1, step2) for cols)."""
+    problem (z1, z2) computes C[cr + m, cc + n] = sum_k A[ar + m, ac + k] * B[br + k, bc + n]
+    (b_kmajor: B[br + n, bc + k]), each coordinate given as ((base, step1, step2) for rows,
+    (base, step1, step2) for cols)."""
     torch = _torch()
     _need(A, torch.float16, A.shape, "A")
     _need(B, torch.float16, B.shape, "B")
@@ -346,6 +348,7 @@ def gmm_batched(A, B, C, M: int, N: int, K: int, z: tuple, a: tuple, b: tuple, c
     for name, (rows, cols) in zip("abc", (a, b, c)):
         getattr(d, f"{name}_row")[:] = rows
         getattr(d, f"{name}_col")[:] = cols
+    d.b_kmajor = int(bool(b_kmajor))
     epi = _epilogue(bias, relu, N, A.device, residual, tuple(C.shape))
     _check(lib().tir_b200_gmm_batched(_ptr(A), A.shape[0], A.shape[1], _ptr(B), B.shape[0], B.shape[1],
                                       _ptr(C), C.shape[0], C.shape[1], M, N, K, ctypes.byref(d),

@@ -115,6 +115,8 @@ struct alignas(64) IgemmParams {
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
   int32_t batch_tiles;  // batched GMM: tiles per problem (0 = not batched)
+  int32_t b_kmajor;     // B given as [N rows, K cols] (K contiguous): K-major UMMA operand, SW128
+                        // boxes {64 K, BN rows} (attention's Q K^T reads K straight from QKV)
   int32_t batch_z2;     // problems per z1
   BatchAxis ba, bb, bc; // A / B / C coordinates per problem
 };
@@ -317,9 +319,12 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     for (int j = pw; j < pps; j += kProducers) my_tx += piece_bytes;
     if (b_mode == B_PIECES)
       for (int j = pw; j < pps; j += kProducers) my_tx += kBChunks * box * Cfg::kBRowBytes;
-    if (b_mode == B_STREAM)
+    if (b_mode == B_STREAM && !p.b_kmajor)
       for (int ch = 0; ch < kBChunks; ++ch)
         if ((pps + ch) % kProducers == pw) my_tx += kBChunkBytes;
+    if (b_mode == B_STREAM && p.b_kmajor)
+      for (int u = 0; u < KS; ++u)
+        if ((pps + u) % kProducers == pw) my_tx += BN * 128;
     if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
       // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once.
       int s0, mt0, g0, nt0;
@@ -400,12 +405,18 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
                             col0 + ch * Cfg::kBChunk, e.w);
             }
           }
-          if (b_mode == B_STREAM) {
+          if (b_mode == B_STREAM && !p.b_kmajor) {
 #pragma unroll
             for (int ch = 0; ch < kBChunks; ++ch)
               if ((pps + ch) % kProducers == pw)
                 tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk + b_c,
                             st * Cfg::kBRows + b_r);
+          } else if (b_mode == B_STREAM) {
+            // K-major B: sub-block u = BN rows (N) x 64 K, 128-byte SW128 rows like A
+#pragma unroll
+            for (int u = 0; u < KS; ++u)
+              if ((pps + u) % kProducers == pw)
+                tma_load_2d(sB + u * BN * 128, &p.tmB, &full[slot], st * Cfg::kBRows + u * kBK + b_c, col0 + b_r);
           }
           if (trace && pw == 0 && it < 128) trace[2 * it + 1] = clock64();
         }
@@ -442,9 +453,13 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     }
     const uint64_t adesc0 = smem_desc(smem_u32(sA0), a_lbo, a_sbo, a_layout);
     const uint32_t b_lbo = b_res ? p.b_res_rows * Cfg::kBRowBytes : Cfg::kBRows * Cfg::kBRowBytes;
-    const uint64_t bdesc0 = smem_desc(smem_u32(sB0), b_lbo, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
-    constexpr uint32_t kBk = (16 * Cfg::kBRowBytes) >> 4;            // per k-step (16 rows)
-    constexpr uint32_t kBsub = (kBK * Cfg::kBRowBytes) >> 4;         // per 64-row sub-block
+    const bool bkm = p.b_kmajor != 0;
+    const uint64_t bdesc0 = bkm ? smem_desc(smem_u32(sB0), 16, 1024, 2)
+                                : smem_desc(smem_u32(sB0), b_lbo, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
+    // per k-step / per 64-deep sub-block descriptor advances (16-byte units)
+    const uint32_t kBk = bkm ? 2u : (16 * Cfg::kBRowBytes) >> 4;
+    const uint32_t kBsub = bkm ? static_cast<uint32_t>(BN * 128) >> 4 : (kBK * Cfg::kBRowBytes) >> 4;
+    const uint32_t idesc = bkm ? idesc_f16_f32(kBM, BN, 0, 0) : Cfg::kIdesc;
     constexpr uint32_t kBst = (Cfg::kBRows * Cfg::kBRowBytes) >> 4;  // per stage (resident)
     constexpr uint32_t kBslot = Cfg::kBBytes >> 4;                   // per ring slot
     constexpr uint32_t kAslot = Cfg::kABytes >> 4;
@@ -476,7 +491,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
 #pragma unroll
             for (int k = 0; k < kBK / 16; ++k)
               umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
-                       Cfg::kIdesc, ((st - st0) | u | k) != 0);
+                       idesc, ((st - st0) | u | k) != 0);
           umma_commit(&empty[slot]);
         }
         __syncwarp();

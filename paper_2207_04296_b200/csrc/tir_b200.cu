@@ -584,7 +584,9 @@ int gmm_batched_impl(const uint16_t* A, int64_t a_rows, int64_t lda, const uint1
     return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: leading dims must be multiples of 8");
   if (epi.residual && !out_f16) return set_err(TIR_B200_ERR_UNSUPPORTED, "gmm_batched: residual needs fp16 C");
   // every problem's windows inside their tensors (checked at the z corners; coordinates are affine in z)
-  const int64_t lim[3][2] = {{a_rows - M, lda - K}, {b_rows - K, ldb - N}, {c_rows - M, ldc - N}};
+  const bool bkm = bt->b_kmajor != 0;
+  const int64_t lim[3][2] = {{a_rows - M, lda - K}, {b_rows - (bkm ? N : K), ldb - (bkm ? K : N)},
+                             {c_rows - M, ldc - N}};
   const int64_t* ax[3][2] = {{bt->a_row, bt->a_col}, {bt->b_row, bt->b_col}, {bt->c_row, bt->c_col}};
   for (int t = 0; t < 3; ++t)
     for (int d = 0; d < 2; ++d)
@@ -606,8 +608,10 @@ int gmm_batched_impl(const uint16_t* A, int64_t a_rows, int64_t lda, const uint1
   const int ks_eff = bn >= 128 ? std::min(ks, 2) : ks;
   int rc = encode_2d(&p.tmA[0], A, a_rows, lda, 64, tb::kBM);
   if (rc) return rc;
-  rc = encode_2d(&p.tmB, B, b_rows, ldb, std::min(bn, 64), tb::kBK * ks_eff);
+  // MN-major B: boxes {min(BN, 64) cols, KS*64 rows}; K-major: {64 K, BN rows}
+  rc = bkm ? encode_2d(&p.tmB, B, b_rows, ldb, 64, bn) : encode_2d(&p.tmB, B, b_rows, ldb, std::min(bn, 64), tb::kBK * ks_eff);
   if (rc) return rc;
+  p.b_kmajor = bkm ? 1 : 0;
   p.num_sub = 1;
   tb::SubProb& s = p.sub[0];
   set_sub_identity(s);

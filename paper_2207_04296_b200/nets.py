@@ -232,9 +232,9 @@ class DeviceNet:
 
 def launches_per_forward(net) -> int:
     """Kernel launches of one forward (CI % 8 != 0 stems add the two relayout kernels;
-    a BERT layer is 10 launches)."""
+    a BERT layer is 9 launches)."""
     if isinstance(net, BertDef):
-        return 10 * net.layers
+        return 9 * net.layers
     n = 0
     for op in net.ops:
         n += 1
@@ -256,8 +256,8 @@ def build_shard(name: str, global_batch: int, rank: int, world: int, **kw):
 @dataclass
 class BertDef:
     """BERT encoder stack (post-LN, GELU FFN) on fp16 hidden states [B*S, H]:
-    per layer QKV GEMM (+bias) -> K^T relayout -> batched Q K^T over (sequence,
-    head) -> softmax(scale) -> batched P V -> output GEMM (+bias +residual) ->
+    per layer QKV GEMM (+bias) -> batched Q K^T over (sequence, head), K read
+    in place from QKV as a K-major operand -> softmax(scale) -> batched P V -> output GEMM (+bias +residual) ->
     LayerNorm -> FFN GEMM (+bias, GELU) -> GEMM (+bias +residual) -> LayerNorm.
     The token embedding lookup is not part of the operator graph: the input is
     the embedded hidden-state tensor."""
@@ -324,7 +324,6 @@ class DeviceBert:
         e = lambda *s: torch.empty(s, dtype=torch.float16, device=device)  # noqa: E731
         self.x = e(t, h)          # layer input / output (hidden states)
         self.qkv = e(t, 3 * h)
-        self.kt = e(h, t)         # K^T: [hidden, tokens]
         self.scores = e(net.batch * net.heads * net.seq, net.seq)
         self.ctx = e(t, h)
         self.attn = e(t, h)
@@ -349,11 +348,11 @@ class DeviceBert:
         for li in range(lo, net.layers if hi is None else hi):
             w = self.w[li]
             api.gmm(self.x, w["w_qkv"], self.qkv, out_f16=True, bias=w["b_qkv"], stream=st)
-            api.transpose(self.qkv, H, H, self.kt, stream=st)
-            # scores[(b*nh + h)*S + m, n] = Q[b*S + m, h*dh + k] . K^T[h*dh + k, b*S + n]
-            api.gmm_batched(self.qkv, self.kt, self.scores, S, S, dh, (B, nh),
-                            a=((0, S, 0), (0, 0, dh)), b=((0, 0, dh), (0, S, 0)),
-                            c=((0, nh * S, S), (0, 0, 0)), stream=st)
+            # scores[(b*nh + h)*S + m, n] = Q[b*S + m, h*dh + k] . K[b*S + n, H + h*dh + k]
+            # (K read straight from QKV as a K-major B operand: no transpose)
+            api.gmm_batched(self.qkv, self.qkv, self.scores, S, S, dh, (B, nh),
+                            a=((0, S, 0), (0, 0, dh)), b=((0, S, 0), (H, 0, dh)),
+                            c=((0, nh * S, S), (0, 0, 0)), b_kmajor=True, stream=st)
             api.softmax(self.scores, 1.0 / math.sqrt(dh), Y=self.scores, stream=st)
             # ctx[b*S + m, h*dh + n] = P[(b*nh + h)*S + m, k] . V[b*S + k, 2H + h*dh + n]
             api.gmm_batched(self.scores, self.qkv, self.ctx, S, dh, S, (B, nh),

@@ -169,6 +169,33 @@ def test_gmm_batched_strided_heads(n_dim, cuda):
             assert (got - want).abs().max().item() <= 2e-3 * want.abs().max().item() + 1e-2
 
 
+def test_gmm_batched_kmajor_b(cuda):
+    """B given as [N, K] (K contiguous): attention's K read in place from QKV."""
+    g = torch.Generator(device=cuda).manual_seed(8)
+    B, nh, S, dh = 2, 3, 128, 64
+    H = nh * dh
+    qkv = torch.randn(B * S, 3 * H, device=cuda, generator=g).half()
+    out = torch.zeros(B * nh * S, S, device=cuda).half()
+    tb.gmm_batched(qkv, qkv, out, S, S, dh, (B, nh), a=((0, S, 0), (0, 0, dh)), b=((0, S, 0), (H, 0, dh)),
+                   c=((0, nh * S, S), (0, 0, 0)), b_kmajor=True)
+    for b in range(B):
+        for h in range(nh):
+            q = qkv[b * S:(b + 1) * S, h * dh:(h + 1) * dh].double()
+            k = qkv[b * S:(b + 1) * S, H + h * dh:H + (h + 1) * dh].double()
+            want = q @ k.t()
+            got = out[(b * nh + h) * S:(b * nh + h + 1) * S].double()
+            assert (got - want).abs().max().item() <= 2e-3 * want.abs().max().item() + 1e-2
+    # wider K (two 64-deep sub-blocks) and N = 256 tiles
+    a = torch.randn(2 * 256, 128, device=cuda, generator=g).half()
+    bt = torch.randn(2 * 256, 128, device=cuda, generator=g).half()
+    c = torch.zeros(2 * 256, 256, device=cuda).half()
+    tb.gmm_batched(a, bt, c, 256, 256, 128, (2, 1), a=((0, 256, 0), (0, 0, 0)), b=((0, 256, 0), (0, 0, 0)),
+                   c=((0, 256, 0), (0, 0, 0)), b_kmajor=True)
+    for z in range(2):
+        want = a[z * 256:(z + 1) * 256].double() @ bt[z * 256:(z + 1) * 256].double().t()
+        assert (c[z * 256:(z + 1) * 256].double() - want).abs().max().item() <= 2e-3 * want.abs().max().item() + 1e-2
+
+
 def test_gmm_batched_rejects_bad_windows(cuda):
     a = torch.zeros(128, 64, device=cuda).half()
     c = torch.zeros(128, 64, device=cuda).half()

@@ -94,7 +94,7 @@ def test_bert_structure_and_flops():
     assert abs(params / 24 / 12.58e6 - 1) < 0.01
     # per 512-token sequence: dense 2 x 512 x 12.58M x 24 + attention 4 x 16 x 512^2 x 64 x 24
     assert net.flops == 24 * (2 * 512 * (4 * 1024 * 1024 + 2 * 1024 * 4096) + 4 * 16 * 512 * 512 * 64)
-    assert nets.launches_per_forward(net) == 240
+    assert nets.launches_per_forward(net) == 216
 
 
 def test_bert_reference_small():

@@ -18,9 +18,9 @@ st = dn.stream
 T = net.tokens
 ops = [
     ("qkv gmm", 2 * T * H * 3 * H, lambda: api.gmm(dn.x, w["w_qkv"], dn.qkv, out_f16=True, bias=w["b_qkv"], stream=st)),
-    ("K^T transpose", 0, lambda: api.transpose(dn.qkv, H, H, dn.kt, stream=st)),
-    ("QK^T batched", 2 * B * nh * S * S * dh, lambda: api.gmm_batched(dn.qkv, dn.kt, dn.scores, S, S, dh, (B, nh),
-        a=((0, S, 0), (0, 0, dh)), b=((0, 0, dh), (0, S, 0)), c=((0, nh * S, S), (0, 0, 0)), stream=st)),
+    ("QK^T batched", 2 * B * nh * S * S * dh, lambda: api.gmm_batched(dn.qkv, dn.qkv, dn.scores, S, S, dh, (B, nh),
+        a=((0, S, 0), (0, 0, dh)), b=((0, S, 0), (H, 0, dh)), c=((0, nh * S, S), (0, 0, 0)), b_kmajor=True,
+        stream=st)),
     ("softmax", 0, lambda: api.softmax(dn.scores, 1 / math.sqrt(dh), Y=dn.scores, stream=st)),
     ("PV batched", 2 * B * nh * S * S * dh, lambda: api.gmm_batched(dn.scores, dn.qkv, dn.ctx, S, dh, S, (B, nh),
         a=((0, nh * S, S), (0, 0, 0)), b=((0, S, 0), (2 * H, 0, dh)), c=((0, S, 0), (0, 0, dh)), stream=st)),
