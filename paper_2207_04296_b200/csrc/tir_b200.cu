@@ -310,7 +310,8 @@ bool use_epi8(const tb::IgemmParams& p, int bn, int ks) {
   const bool fused = p.out_f16 || p.bias || p.relu || p.residual;
   // up to K = 1024 per tile (measured on BERT-large: QKV / out / FFN1 GEMMs -5 / -5 / -22 %,
   // FFN2 with K = 4096 +3 %)
-  return p.ksplit <= 1 && nst * ks * tb::kBK <= 1024 && bn >= 64 && fused;
+  // narrow im2col pieces (< 64 channels) are TMA-request-bound: keep 4 producers
+  return p.ksplit <= 1 && nst * ks * tb::kBK <= 1024 && bn >= 64 && fused && p.a_box_ch == 64;
 }
 
 template <int BN>
