@@ -28,6 +28,9 @@
 //   warp 8      TMEM allocator + MMA issuer: 4 x tcgen05.mma.kind::f16
 //               (M=128, N=BN, K=16) per stage into a TMEM fp32 accumulator;
 //               tcgen05.commit frees the slot / publishes the accumulator
+// The EPI8 instantiation (384 threads: 8 epilogue + 3 producer + 1 MMA warps,
+// IgemmCfg) splits each tile's columns over two epilogue warps per TMEM
+// sub-partition; the host picks it for short-K fused tiles (use_epi8).
 //
 // K enumeration (must match the reference reduction domain, workloads.h:106-108):
 // k = tap * CIg + c with tap = (kd, kh, kw) row-major and c fastest, i.e. the

@@ -266,7 +266,7 @@ def test_native_kernels_actually_launch(cuda):
     assert tb.launch_count() == 2
 
 
-@pytest.mark.parametrize("variant", ["TIR_B200_TAPN", "TIR_B200_HALO_LINEAR", "TIR_B200_PAIR"])
+@pytest.mark.parametrize("variant", ["TIR_B200_TAPN", "TIR_B200_HALO_LINEAR", "TIR_B200_PAIR", "TIR_B200_STORE256"])
 def test_opt_in_halo_variants_exact(variant, monkeypatch, cuda):
     """The measured-and-rejected halo variants (tap-packed N, linear tiles) stay
     correct: bit-exact on the reference distribution, with bias + ReLU and fp16
