@@ -173,9 +173,106 @@ __global__ void __launch_bounds__(256) pack_kw_fused_kernel(
   }
 }
 
+// Window form of the (kw, c) packing, for sw % dw == 0 (every stride-1 conv, and
+// DIL / C3D's strided stems): stage S[q] = X[row, q*dw - pw, 0:c] (zero out of
+// bounds) per input row; then output pixel o's packed vector is the CONTIGUOUS
+// run S[o*(sw/dw) .. +kw) of kwc halves, followed by cp - kwc zeros. Each thread
+// emits one 16-byte output vector from five aligned 32-bit shared loads and a
+// funnel shift (no per-element gathers or index tables: the gather form spent
+// ~24 shared loads per vector and ran the relayout at ~2.9 TB/s).
+__global__ void __launch_bounds__(256) pack_kw_win_kernel(
+    const uint16_t* __restrict__ x, uint16_t* __restrict__ y, const uint16_t* __restrict__ w,
+    uint16_t* __restrict__ wy, int32_t rows, int32_t rpb, int32_t xblocks, int32_t iw, int32_t c, int32_t ow,
+    int32_t sw_dw, int32_t pw, int32_t dw, int32_t slen, int32_t nstage, int32_t gshift, int32_t khd,
+    int32_t kwc, int32_t co) {
+  extern __shared__ __align__(16) uint16_t sst[];  // rpb rows of slen halves
+  const int32_t cp = 8 << gshift;
+  if (static_cast<int32_t>(blockIdx.x) >= xblocks) {  // weights
+    const int64_t total = static_cast<int64_t>(khd) * cp * co;
+    const int64_t step = static_cast<int64_t>(gridDim.x - xblocks) * blockDim.x;
+    for (int64_t i = (blockIdx.x - xblocks) * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += step) {
+      const int32_t col = static_cast<int32_t>(i % co);
+      const int64_t r = i / co;
+      const int32_t g = static_cast<int32_t>(r / cp), j = static_cast<int32_t>(r % cp);
+      wy[i] = j < kwc ? w[(static_cast<int64_t>(g) * kwc + j) * co + col] : static_cast<uint16_t>(0);
+    }
+    return;
+  }
+  const int32_t row0 = blockIdx.x * rpb;
+  const int32_t nrows = min(rpb, rows - row0);
+  const int32_t row_elems = iw * c;
+  const uint16_t* xr = x + static_cast<int64_t>(row0) * row_elems;
+  // stage: nstage = (ow-1)*(sw/dw)*c + kw*c halves carry data, the rest of slen is zero
+  for (int32_t i = threadIdx.x; i < nrows * slen; i += blockDim.x) {
+    const int32_t r = i / slen, k = i - r * slen;
+    uint16_t v = 0;
+    if (k < nstage) {
+      const int32_t q = k / c, ch = k - q * c;
+      const int32_t col = q * dw - pw;
+      if (col >= 0 && col < iw) v = __ldg(xr + r * row_elems + col * c + ch);
+    }
+    sst[i] = v;
+  }
+  __syncthreads();
+  const uint32_t* s32 = reinterpret_cast<const uint32_t*>(sst);
+  const int32_t nvec = ow << gshift;
+  uint4* yb = reinterpret_cast<uint4*>(y + static_cast<int64_t>(row0) * ow * cp);
+  for (int32_t v = threadIdx.x; v < nrows * nvec; v += blockDim.x) {
+    const int32_t r = v / nvec, vr = v - r * nvec;
+    const int32_t o = vr >> gshift, j0 = (vr & ((1 << gshift) - 1)) * 8;
+    uint4 u = make_uint4(0, 0, 0, 0);
+    if (j0 < kwc) {
+      const int32_t s = r * slen + o * sw_dw * c + j0;  // halves; slen is even
+      const uint32_t* p = s32 + (s >> 1);
+      uint32_t a[5];
+#pragma unroll
+      for (int i = 0; i < 5; ++i) a[i] = p[i];
+      uint32_t o4[4];
+      const uint32_t sh = (s & 1) * 16;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        uint32_t word = __funnelshift_r(a[i], a[i + 1], sh);
+        const int32_t jl = j0 + 2 * i;
+        if (jl >= kwc) word = 0;
+        else if (jl + 1 >= kwc) word &= 0xffffu;
+        o4[i] = word;
+      }
+      u = make_uint4(o4[0], o4[1], o4[2], o4[3]);
+    }
+    yb[v] = u;
+  }
+}
+
+inline int launch_pack_kw_win(const uint16_t* x, uint16_t* y, const uint16_t* w, uint16_t* wy, int64_t rows,
+                              int64_t iw, int64_t c, int64_t ow, int64_t kw, int64_t sw, int64_t pw, int64_t dw,
+                              int64_t cp, int64_t khd, int64_t kwc, int64_t co, cudaStream_t st) {
+  if (dw < 1 || sw % dw != 0 || cp > 64 || cp < 8 || rows >= (1ll << 30)) return 2;
+  const int64_t sw_dw = sw / dw;
+  const int64_t nstage = ((ow - 1) * sw_dw + kw) * c;
+  // reads reach 8*ceil(kwc/8) + 2 halves past a window start
+  const int64_t slen = ((ow - 1) * sw_dw * c + (kwc + 7) / 8 * 8 + 2 + 7) / 8 * 8;
+  if (slen * 2 > 24 * 1024) return 2;
+  const int rpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 12 * 1024 / (slen * 2))));
+  const int64_t xblocks = (rows + rpb - 1) / rpb;
+  const int wblocks = 16;
+  const int gshift = cp == 8 ? 0 : cp == 16 ? 1 : cp == 32 ? 2 : 3;
+  const size_t smem = static_cast<size_t>(rpb * slen * 2);
+  pack_kw_win_kernel<<<static_cast<unsigned>(xblocks + wblocks), 256, smem, st>>>(
+      x, y, w, wy, static_cast<int32_t>(rows), rpb, static_cast<int32_t>(xblocks), static_cast<int32_t>(iw),
+      static_cast<int32_t>(c), static_cast<int32_t>(ow), static_cast<int32_t>(sw_dw), static_cast<int32_t>(pw),
+      static_cast<int32_t>(dw), static_cast<int32_t>(slen), static_cast<int32_t>(nstage), gshift,
+      static_cast<int32_t>(khd), static_cast<int32_t>(kwc), static_cast<int32_t>(co));
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 inline int launch_pack_kw_fused(const uint16_t* x, uint16_t* y, const uint16_t* w, uint16_t* wy, int64_t rows,
                                 int64_t iw, int64_t c, int64_t ow, int64_t kw, int64_t sw, int64_t pw, int64_t dw,
                                 int64_t cp, int64_t khd, int64_t kwc, int64_t co, cudaStream_t st) {
+  if (!getenv("TIR_B200_PACK_GATHER")) {
+    const int rc = launch_pack_kw_win(x, y, w, wy, rows, iw, c, ow, kw, sw, pw, dw, cp, khd, kwc, co, st);
+    if (rc != 2) return rc;
+  }
   const int64_t row_bytes = iw * c * 2;
   if (row_bytes > 48 * 1024 || rows >= (1ll << 30) || cp > 64) return 2;  // caller falls back
   const int rpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 12 * 1024 / row_bytes)));

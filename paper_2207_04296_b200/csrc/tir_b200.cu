@@ -268,6 +268,10 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
                    p.cog % 32 == 0 &&
                    (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0 && !getenv("TIR_B200_NO_SMEM_BIAS"))
                       ? (nbias + 3) / 4 * 4 : 0;
+  // the staged bias must not cost the ring its second stage
+  if (p.bias_floats && di.smem_optin - 1280 - table - p.bias_floats * 4 - Cfg::kEpiBytes <
+                           2 * (Cfg::kABytes + Cfg::kBBytes))
+    p.bias_floats = 0;
   const int budget = di.smem_optin - 1024 - 256 - table - p.bias_floats * 4 - Cfg::kEpiBytes;
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
@@ -337,14 +341,18 @@ int launch_igemm(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
 
 // K sub-blocks (64 deep) per pipeline stage: the largest of {4, 2, 1} whose
 // padding waste (pieces past the end of the reduction) is minimal, capped by
-// shared memory (two stages of A + B must fit).
+// shared memory (two stages of A + B must fit). Narrow-piece convs (box < 64
+// channels: the packed CI = 3 stems) never take the 8-warp epilogue, so their
+// two stages may use everything but the 4-warp staging (DIL: one 256-deep stage
+// per tile instead of two, 36.9 -> 34.9 us).
 int choose_ks(int max_pieces, int box, int bn) {
   if (const char* e = getenv("TIR_B200_KS")) return std::max(1, std::min(4, atoi(e)));
   const int pps1 = tb::kBK / box;
+  const int limit = box < 64 ? 227 * 1024 - 1280 - 4 * 8192 - 16 * max_pieces - 512 : 190 * 1024;
   int best = 1;
   int64_t best_waste = -1;
   for (int ks : {4, 2, 1}) {
-    if (2 * ks * (16384 + 64 * bn * 2) > 190 * 1024) continue;  // two stages must fit
+    if (2 * ks * (16384 + 64 * bn * 2) > limit) continue;  // two stages must fit
     const int64_t per = static_cast<int64_t>(pps1) * ks;
     const int64_t waste = (max_pieces + per - 1) / per * per - max_pieces;
     if (waste * 8 <= max_pieces) return ks;  // <= 12.5% padded MMA work: deepest such stage
