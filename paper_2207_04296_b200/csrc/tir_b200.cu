@@ -253,6 +253,24 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 
 // ------------------------------------------------------------------ igemm launch
 
+// B-multicast pairs: tiled A, streamed row-major B in >= 2 chunks, one problem
+// (no groups / split-K / batch / sub-problems) and an even M-tile count. Taken
+// by default for large K-heavy GEMMs only (>= 4 waves, K >= 2048). Measured on
+// B200: 8192^3 1156 -> 1200 TFLOPS, while single-wave and K = 1024 GEMMs gain
+// nothing (their per-SM L2 reads are not the limit).
+bool use_mc(const tb::IgemmParams& p, int bn, int ks, int sms) {
+  const char* mc_env = getenv("TIR_B200_MC");  // read per launch (tests toggle it)
+  const int env = mc_env ? atoi(mc_env) : -1;
+  if (env == 0) return false;
+  const bool ok = p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
+                  p.groups == 1 && p.ksplit == 1 && !p.batch_tiles && bn >= 128 && p.sub[0].tiles_m % 2 == 0 &&
+                  p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
+  if (!ok) return false;
+  if (env == 1) return true;
+  const int64_t k = static_cast<int64_t>(p.sub[0].num_stages) * ks * tb::kBK;
+  return p.total_tiles >= 4 * sms && k >= 2048;
+}
+
 template <int BN, int KS, bool EPI8>
 int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   using Cfg = tb::IgemmCfg<BN, KS, EPI8>;
@@ -295,9 +313,40 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces, p.bias_floats);
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
-  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
+  // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
+  p.mc = 0;
+  if (use_mc(p, BN, KS, di.sms) && grid >= 2) {
+    static int max_clusters = -1;  // per instantiation: same smem / block for every launch that gets here
+    if (max_clusters < 0) {
+      cudaLaunchConfig_t cfg{};
+      cfg.gridDim = dim3(di.sms / 2 * 2);
+      cfg.blockDim = dim3(Cfg::kThreadsN);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      max_clusters = cudaOccupancyMaxActiveClusters(&n, tb::igemm_tc_kernel<BN, KS, EPI8>, &cfg) == cudaSuccess
+                         ? n : 0;
+      cudaGetLastError();
+    }
+    if (max_clusters > 0) {
+      p.mc = 1;
+      grid = std::min(grid / 2, max_clusters) * 2;
+    }
+  }
+  if (const char* e = getenv("TIR_B200_MAX_CTAS"))
+    grid = p.mc ? std::max(2, std::min(grid, atoi(e) / 2 * 2)) : std::max(1, std::min(grid, atoi(e)));
   p.trace = g_trace;
-  CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, Cfg::kThreadsN, smem, stream, p));
+  if (p.mc) {
+    CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, 2, Cfg::kThreadsN, smem, stream, p));
+  } else {
+    CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, Cfg::kThreadsN, smem, stream, p));
+  }
   ++g_launches;
   return TIR_B200_OK;
 }

@@ -216,6 +216,36 @@ def test_gmm_d2_and_variants(mnk, cuda):
     assert np.mean(got16 == c16) > 0.99
 
 
+@pytest.mark.parametrize("mnk", [(1024, 1024, 1024), (2048, 512, 2048), (384, 256, 256), (4096, 1024, 4096)],
+                         ids=lambda t: "x".join(map(str, t)))
+def test_gmm_b_multicast_pairs(mnk, monkeypatch, cuda):
+    """B-multicast CTA pairs (igemm.cuh mc_tile; forced with TIR_B200_MC=1, default for
+    large K-heavy GEMMs) give bit-identical results to the unpaired kernel — same MMAs
+    in the same order — plain and with the fused bias / GELU / residual fp16 epilogue,
+    and bit-exact vs the oracle on the reference distribution. 384 rows = 3 M tiles
+    (odd) falls back to unpaired launches."""
+    import torch
+
+    M, N, K = mnk
+    a = O.reference_tensor((M, K), 1)
+    b = O.reference_tensor((K, N), 2)
+    an, bn_ = O.normal_f16((M, K), 3), O.normal_f16((K, N), 4)
+    bias = torch.randn(N, device=cuda)
+    res = torch.randn(M, N, device=cuda).half()
+    outs = {}
+    for mc in ("0", "1"):
+        monkeypatch.setenv("TIR_B200_MC", mc)
+        outs[mc] = (tb.gmm(dev(a, cuda), dev(b, cuda)), tb.gmm(dev(an, cuda), dev(bn_, cuda)),
+                    tb.gmm(dev(an, cuda), dev(bn_, cuda), out_f16=True, bias=bias, relu="gelu", residual=res))
+    torch.cuda.synchronize()
+    for x, y in zip(outs["0"], outs["1"]):
+        assert torch.equal(x, y)
+    rows = 128
+    c = outs["1"][0].cpu().numpy()
+    assert O.tensors_bitwise_equal(c[:rows], O.gmm(a[:rows], b, threads=8))
+    assert O.tensors_bitwise_equal(c[-rows:], O.gmm(a[-rows:], b, threads=8))
+
+
 def test_gmm_unsupported_and_value_errors(cuda):
     import torch
 
