@@ -225,6 +225,45 @@ __device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
       : "memory");
 }
 
+// p.mc == 2: the pair runs tcgen05.mma.cta_group::2 (M = 256, the leader issues
+// for both CTAs). Each CTA loads its own A and HALF of B's columns (no
+// multicast), so per-SM shared-memory fill and MMA operand reads both drop to
+// A + B/2; TMA loads complete on the leader's full barrier, commits multicast.
+__device__ __forceinline__ uint32_t mc_leader_addr(const void* q) { return smem_u32(q) & 0xFEFFFFFFu; }
+
+__device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* m, uint32_t leader_bar, int c0,
+                                                int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(leader_bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_f16_cg2(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void umma_commit_cg2(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(static_cast<uint16_t>(3))
+      : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_rank0(uint64_t* bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(smem_u32(bar)));
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+
 __device__ __forceinline__ void mc_cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -262,7 +301,9 @@ __device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& 
   return e;
 }
 
-template <int BN, int KS, bool EPI8 = false>
+// CG2 instantiations (p.mc == 2) contain cta_group::2 instructions and must be
+// launched as clusters of 2; every other launch uses CG2 = false.
+template <int BN, int KS, bool EPI8 = false, bool CG2 = false>
 __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     igemm_tc_kernel(const __grid_constant__ IgemmParams p) {
   using Cfg = IgemmCfg<BN, KS, EPI8>;
@@ -291,6 +332,9 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   constexpr uint32_t kMmaWarp = Cfg::kMma;
+  int mc_rank = 0;
+  if (p.mc) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(mc_rank));
+  constexpr bool cg2 = CG2;
 
   if (threadIdx.x == 32 * kMmaWarp + 1) {  // descriptor fetches overlap the prologue
     for (int i = 0; i < p.num_sub; ++i) prefetch_tmap(&p.tmA[i]);
@@ -300,18 +344,25 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], kProducers);  // every producer arrives once per stage
-      mbar_init(&empty[i], p.mc ? 2 : 1);  // mc: both CTAs' MMAs release the slot
+      mbar_init(&empty[i], p.mc == 1 ? 2 : 1);  // mc 1: both CTAs' MMAs release the slot
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 32 * kEpi);
+      mbar_init(&tempty[i], cg2 ? 2 * kEpi : 32 * kEpi);  // cg2: one arrive per epilogue warp of the pair
     }
     mbar_init(bres_full, 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) {
-    tmem_alloc(tmem_slot, Cfg::kTmemCols);
-    tmem_relinquish();
+    if constexpr (cg2) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "n"(Cfg::kTmemCols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc(tmem_slot, Cfg::kTmemCols);
+      tmem_relinquish();
+    }
   }
   if (p.bias_floats) {
     pdl_wait();  // the bias may be produced by the preceding kernel
@@ -346,8 +397,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     // completes about one request per ~500 cycles (tools/tmabw.cu), so a stage's
     // requests are spread over four issuers.
     const int pw = static_cast<int>(warp) - kEpi;
-    int mc_rank = 0;
-    if (p.mc) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(mc_rank));
     const int box = p.a_box_ch;
     const int pps = KS * (kBK / box);  // pieces per stage
     const uint32_t piece_bytes = kBM * box * 2;
@@ -361,8 +410,9 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     if (b_mode == B_PIECES)
       for (int j = pw; j < pps; j += kProducers) my_tx += kBChunks * box * Cfg::kBRowBytes;
     if (b_mode == B_STREAM && !p.b_kmajor)
-      for (int ch = 0; ch < kBChunks; ++ch)
+      for (int ch = 0; ch < (cg2 ? kBChunks / 2 : kBChunks); ++ch)
         if ((pps + ch) % kProducers == pw) my_tx += kBChunkBytes;
+    if constexpr (cg2) my_tx *= 2;  // the leader's barrier receives both CTAs' (identical) shares
     if (b_mode == B_STREAM && p.b_kmajor)
       for (int u = 0; u < KS; ++u)
         if ((pps + u) % kProducers == pw) my_tx += BN * 128;
@@ -415,6 +465,18 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
           if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();
           uint8_t* sA = sA0 + slot * Cfg::kABytes;
           uint8_t* sB = sB0 + slot * Cfg::kBBytes;
+          if constexpr (cg2) {
+            // both CTAs' loads complete on the leader's barrier; only its producers arrive
+            if (mc_rank == 0) mbar_arrive_expect_tx(&full[slot], my_tx);
+            const uint32_t lbar = mc_leader_addr(&full[slot]);
+            for (int j = pw; j < pps; j += kProducers)
+              tma_load_2d_cg2(sA + j * piece_bytes, tmA, lbar, (st * pps + j) * kBK, m0);
+#pragma unroll
+            for (int ch = 0; ch < kBChunks / 2; ++ch)
+              if ((pps + ch) % kProducers == pw)
+                tma_load_2d_cg2(sB + ch * kBChunkBytes, &p.tmB, lbar,
+                                col0 + mc_rank * (BN / 2) + ch * Cfg::kBChunk, st * Cfg::kBRows);
+          } else {
           if (my_tx) mbar_arrive_expect_tx(&full[slot], my_tx);
           else mbar_arrive(&full[slot]);
           for (int j = pw; j < pps; j += kProducers) {
@@ -464,6 +526,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
               if ((pps + u) % kProducers == pw)
                 tma_load_2d(sB + u * BN * 128, &p.tmB, &full[slot], st * Cfg::kBRows + u * kBK + b_c, col0 + b_r);
           }
+          }  // !cg2
           if (trace && pw == 0 && it < 128) trace[2 * it + 1] = clock64();
         }
         __syncwarp();
@@ -516,7 +579,10 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     }
     uint32_t slot = 0, phase = 0, acc = 0, acc_phase = 0;
     int it = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+    const uint32_t idesc_mma = cg2 ? idesc_f16_f32(2 * kBM, BN, 0, 1) : idesc;
+    // cg2: the leader issues every MMA of the pair; the peer's MMA warp idles
+    for (int tile = blockIdx.x + ((cg2 && mc_rank) ? p.total_tiles : 0); tile < p.total_tiles;
+         tile += gridDim.x) {
       int s, mt, g, nt, ks, z1, z2, lt = mc_tile(p, tile);
       split_batch(p, lt, z1, z2);
       decompose_tile(p, lt, s, mt, g, nt, ks);
@@ -535,10 +601,16 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
 #pragma unroll
           for (int u = 0; u < KS; ++u)
 #pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
-                       idesc, ((st - st0) | u | k) != 0);
-          if (p.mc) umma_commit_mc(&empty[slot], 3);
+            for (int k = 0; k < kBK / 16; ++k) {
+              if constexpr (cg2)
+                umma_f16_cg2(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk, idesc_mma,
+                             ((st - st0) | u | k) != 0);
+              else
+                umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
+                         idesc, ((st - st0) | u | k) != 0);
+            }
+          if constexpr (cg2) umma_commit_cg2(&empty[slot]);
+          else if (p.mc) umma_commit_mc(&empty[slot], 3);
           else umma_commit(&empty[slot]);
         }
         __syncwarp();
@@ -548,7 +620,10 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
           phase ^= 1;
         }
       }
-      if (elect_one()) umma_commit(&tfull[acc]);
+      if (elect_one()) {
+        if constexpr (cg2) umma_commit_cg2(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
+      }
       __syncwarp();
       if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
         acc = 0;
@@ -701,7 +776,15 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         }
         if (trace && threadIdx.x == 0 && local < 64) trace[513 + 2 * local] = clock64();
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (cg2) {  // one arrive per warp on the leader's barrier
+          __syncwarp();
+          if (lane == 0) {
+            if (mc_rank == 0) mbar_arrive(&tempty[acc]);
+            else mbar_arrive_rank0(&tempty[acc]);
+          }
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
         if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
           acc = 0;
           acc_phase ^= 1;
@@ -824,7 +907,15 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         }
         if (trace && threadIdx.x == 0 && local < 64) trace[513 + 2 * local] = clock64();
         tc_fence_before();
-        mbar_arrive(&tempty[acc]);
+        if constexpr (cg2) {  // one arrive per warp on the leader's barrier
+          __syncwarp();
+          if (lane == 0) {
+            if (mc_rank == 0) mbar_arrive(&tempty[acc]);
+            else mbar_arrive_rank0(&tempty[acc]);
+          }
+        } else {
+          mbar_arrive(&tempty[acc]);
+        }
         if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
           acc = 0;
           acc_phase ^= 1;
@@ -836,7 +927,14 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == kMmaWarp) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if constexpr (cg2) mc_cluster_sync();  // the leader's MMAs into this CTA's TMEM are done
+  if (warp == kMmaWarp) {
+    if constexpr (cg2)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols)
+                   : "memory");
+    else
+      tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  }
   if (p.mc) mc_cluster_sync();  // no multicast or remote arrive still targets this CTA
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
     uint64_t t_end;

@@ -253,22 +253,19 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 
 // ------------------------------------------------------------------ igemm launch
 
-// B-multicast pairs: tiled A, streamed row-major B in >= 2 chunks, one problem
-// (no groups / split-K / batch / sub-problems) and an even M-tile count. Taken
-// by default for large K-heavy GEMMs only (>= 4 waves, K >= 2048). Measured on
-// B200: 8192^3 1156 -> 1200 TFLOPS, while single-wave and K = 1024 GEMMs gain
-// nothing (their per-SM L2 reads are not the limit).
-bool use_mc(const tb::IgemmParams& p, int bn, int ks, int sms) {
+// CTA pairs for plain GEMMs: tiled A, streamed row-major B in >= 2 chunks, one
+// problem (no groups / split-K / batch / sub-problems), an even M-tile count.
+// Default: tcgen05.mma.cta_group::2 (p.mc = 2; each SM loads and reads half of
+// B). Measured on B200, vs unpaired: 8192^3 1094 -> 1287 TFLOPS, BERT-large
+// QKV / FFN1 / FFN2 / out GEMMs -11 / -12 / -15 / -5 %. TIR_B200_CG2=0 keeps the
+// pairs but only multicasts B (p.mc = 1: +4-7 % at 8192^3, nothing below);
+// TIR_B200_MC=0 disables pairs, TIR_B200_MC=1 forces them.
+bool use_mc(const tb::IgemmParams& p, int bn) {
   const char* mc_env = getenv("TIR_B200_MC");  // read per launch (tests toggle it)
-  const int env = mc_env ? atoi(mc_env) : -1;
-  if (env == 0) return false;
-  const bool ok = p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
-                  p.groups == 1 && p.ksplit == 1 && !p.batch_tiles && bn >= 128 && p.sub[0].tiles_m % 2 == 0 &&
-                  p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
-  if (!ok) return false;
-  if (env == 1) return true;
-  const int64_t k = static_cast<int64_t>(p.sub[0].num_stages) * ks * tb::kBK;
-  return p.total_tiles >= 4 * sms && k >= 2048;
+  if (mc_env && atoi(mc_env) == 0) return false;
+  return p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
+         p.groups == 1 && p.ksplit == 1 && !p.batch_tiles && bn >= 128 && p.sub[0].tiles_m % 2 == 0 &&
+         p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
 }
 
 template <int BN, int KS, bool EPI8>
@@ -315,7 +312,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
                                 static_cast<int>(smem)));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
   p.mc = 0;
-  if (use_mc(p, BN, KS, di.sms) && grid >= 2) {
+  if (use_mc(p, BN) && grid >= 2) {
     static int max_clusters = -1;  // per instantiation: same smem / block for every launch that gets here
     if (max_clusters < 0) {
       cudaLaunchConfig_t cfg{};
@@ -335,14 +332,23 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
       cudaGetLastError();
     }
     if (max_clusters > 0) {
-      p.mc = 1;
+      // 2: tcgen05.mma.cta_group::2 (M = 256, B split by column); 1: B multicast only
+      const char* cg2 = getenv("TIR_B200_CG2");
+      p.mc = (BN >= 128 && !(cg2 && atoi(cg2) == 0)) ? 2 : 1;
       grid = std::min(grid / 2, max_clusters) * 2;
     }
   }
   if (const char* e = getenv("TIR_B200_MAX_CTAS"))
     grid = p.mc ? std::max(2, std::min(grid, atoi(e) / 2 * 2)) : std::max(1, std::min(grid, atoi(e)));
   p.trace = g_trace;
-  if (p.mc) {
+  if (p.mc == 2) {
+    if constexpr (BN >= 128) {
+      CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8, true>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8, true>, grid, 2, Cfg::kThreadsN, smem, stream,
+                                  p));
+    }
+  } else if (p.mc) {
     CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, 2, Cfg::kThreadsN, smem, stream, p));
   } else {
     CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, Cfg::kThreadsN, smem, stream, p));
