@@ -169,9 +169,9 @@ struct IgemmCfg {
   static constexpr int kEpiWarpBytes = 8192;
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
   // smem: [A ring][B ring | resident panel][epilogue staging][piece table][barriers]
-  static size_t smem_bytes(int stages, int b_res_rows, int pieces, int bias_floats) {
+  static size_t smem_bytes(int stages, int b_res_rows, int pieces, int bias_floats, bool cg2 = false) {
     const size_t b = b_res_rows ? static_cast<size_t>(b_res_rows) * BN * 2
-                                : static_cast<size_t>(stages) * kBBytes;
+                                : static_cast<size_t>(stages) * (cg2 ? kBBytes / 2 : kBBytes);
     return 1024 /*align slack*/ + static_cast<size_t>(stages) * kABytes + b + kEpiBytes +
            static_cast<size_t>(pieces) * sizeof(int4) + static_cast<size_t>(bias_floats) * 4 + 256 /*barriers*/;
   }
@@ -314,10 +314,11 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
                                              ~static_cast<uintptr_t>(1023));
   const int S = p.stages;
   const bool b_res = p.b_mode == B_RESIDENT;
+  constexpr int kBSlotBytes = CG2 ? Cfg::kBBytes / 2 : Cfg::kBBytes;  // cg2: this CTA's half of B
   uint8_t* sA0 = smem;
   uint8_t* sB0 = smem + static_cast<size_t>(S) * Cfg::kABytes;
   const size_t b_bytes = b_res ? static_cast<size_t>(p.b_res_rows) * BN * 2
-                               : static_cast<size_t>(S) * Cfg::kBBytes;
+                               : static_cast<size_t>(S) * kBSlotBytes;
   uint8_t* epi_smem = sB0 + b_bytes;  // 1024-aligned (all preceding sizes are)
   int4* pieces = reinterpret_cast<int4*>(epi_smem + Cfg::kEpiBytes);
   // staged fp32 bias (p.bias_floats columns; 0 = read from global with shuffles)
@@ -464,7 +465,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         if (elect_one()) {
           if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();
           uint8_t* sA = sA0 + slot * Cfg::kABytes;
-          uint8_t* sB = sB0 + slot * Cfg::kBBytes;
+          uint8_t* sB = sB0 + slot * kBSlotBytes;
           if constexpr (cg2) {
             // both CTAs' loads complete on the leader's barrier; only its producers arrive
             if (mc_rank == 0) mbar_arrive_expect_tx(&full[slot], my_tx);
@@ -570,7 +571,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     const uint32_t kBsub = bkm ? static_cast<uint32_t>(BN * 128) >> 4 : (kBK * Cfg::kBRowBytes) >> 4;
     const uint32_t idesc = bkm ? idesc_f16_f32(kBM, BN, 0, 0) : Cfg::kIdesc;
     constexpr uint32_t kBst = (Cfg::kBRows * Cfg::kBRowBytes) >> 4;  // per stage (resident)
-    constexpr uint32_t kBslot = Cfg::kBBytes >> 4;                   // per ring slot
+    constexpr uint32_t kBslot = kBSlotBytes >> 4;                    // per ring slot
     constexpr uint32_t kAslot = Cfg::kABytes >> 4;
     constexpr uint32_t kAsub = Cfg::kSubA >> 4;
     if (b_res && static_cast<int>(blockIdx.x) < p.total_tiles) {

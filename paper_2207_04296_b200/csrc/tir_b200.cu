@@ -307,7 +307,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes));
   }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
-  const size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces, p.bias_floats);
+  size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces, p.bias_floats);
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
@@ -337,6 +337,10 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
       p.mc = (BN >= 128 && !(cg2 && atoi(cg2) == 0)) ? 2 : 1;
       grid = std::min(grid / 2, max_clusters) * 2;
     }
+  }
+  if (p.mc == 2) {  // half of B per slot: a deeper ring in the same shared memory
+    p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes / 2));
+    smem = Cfg::smem_bytes(p.stages, 0, p.total_pieces, p.bias_floats, true);
   }
   if (const char* e = getenv("TIR_B200_MAX_CTAS"))
     grid = p.mc ? std::max(2, std::min(grid, atoi(e) / 2 * 2)) : std::max(1, std::min(grid, atoi(e)));
