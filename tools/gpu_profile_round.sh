@@ -13,6 +13,11 @@ ncu --set full --clock-control none --import-source on -k regex:"igemm" -s 2 -c 
     -o gpurun_out/${TAG}_full_R50_1x1res python tools/one_gmm.py 100352 64 256 f16_bias_relu_res > /dev/null 2>&1
 ncu --set full --clock-control none --import-source on -k regex:"igemm" -s 2 -c 1 \
     -o gpurun_out/${TAG}_full_BERT_qk python tools/one_bmm.py > /dev/null 2>&1
+# the cta_group::2 GEMM pairs: the 8192^3 sweep line and BERT-large's FFN1 shape
+ncu --set full --clock-control none --import-source on -k regex:"igemm" -s 2 -c 1 \
+    -o gpurun_out/${TAG}_full_GMM8K python tools/one_gmm.py 8192 8192 8192 f32 > /dev/null 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"igemm" -s 2 -c 1 \
+    -o gpurun_out/${TAG}_full_BERT_ffn1 python tools/one_gmm.py 4096 1024 4096 f16_bias > /dev/null 2>&1
 ls -la gpurun_out/*.ncu-rep
 # summarise on the box (the reports are ~12 MB each; only C2D's travels back)
 python tools/ncu_summary.py ${TAG} > gpurun_out/${TAG}_ncu_summary.txt 2>&1
