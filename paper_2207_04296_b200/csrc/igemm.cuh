@@ -120,7 +120,7 @@ struct alignas(64) IgemmParams {
   int32_t batch_tiles;  // batched GMM: tiles per problem (0 = not batched)
   int32_t b_kmajor;     // B given as [N rows, K cols] (K contiguous): K-major UMMA operand, SW128
                         // boxes {64 K, BN rows} (attention's Q K^T reads K straight from QKV)
-  int32_t mc;           // cluster pair sharing B (TMA multicast): see mc_tile
+  int32_t mc;           // 2: cta_group::2 CTA pair (CG2 instantiation, clusters of 2): see mc_tile
   int32_t batch_z2;     // problems per z1
   BatchAxis ba, bb, bc; // A / B / C coordinates per problem
 };
@@ -195,37 +195,22 @@ __device__ __forceinline__ void decompose_tile(const IgemmParams& p, int tile, i
   mt = rest / p.groups;
 }
 
-// B-multicast pairs (p.mc; GMM-shaped launches only: one sub-problem, one group,
-// no split-K or batch, even M-tile count). The grid is clusters of 2 and CTA r
-// of a cluster takes M tile 2*i + r of the same N tile as its peer, so each CTA
-// loads its own A but only half of the B chunks, multicast into both CTAs'
-// rings: per-SM L2 reads per stage drop from A + B to A + B/2. Iteration tile t
+// CTA pairs (CG2; GMM-shaped launches only: one sub-problem, one group, no
+// split-K or batch, even M-tile count). The grid is clusters of 2 and CTA r of a
+// cluster takes M tile 2*i + r of the same N tile as its peer. Iteration tile t
 // (t = blockIdx.x + j * gridDim.x, gridDim even) -> pair t / 2, rank t & 1.
+template <bool CG2>
 __device__ __forceinline__ int mc_tile(const IgemmParams& p, int tile) {
-  if (!p.mc) return tile;
-  const int pt = tile >> 1;
-  const int nt = pt % p.tiles_n, mtp = pt / p.tiles_n;
-  return (2 * mtp + (tile & 1)) * p.tiles_n + nt;
+  if constexpr (!CG2) {
+    return tile;
+  } else {
+    const int pt = tile >> 1;
+    const int nt = pt % p.tiles_n, mtp = pt / p.tiles_n;
+    return (2 * mtp + (tile & 1)) * p.tiles_n + nt;
+  }
 }
 
-__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
-                                               uint16_t mask) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
-      " [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
-      "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
-      : "memory");
-}
-
-// Arrives on `bar` in every CTA of `mask` once this thread's prior MMAs complete.
-__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
-  asm volatile(
-      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          smem_u32(bar)), "h"(mask)
-      : "memory");
-}
-
-// p.mc == 2: the pair runs tcgen05.mma.cta_group::2 (M = 256, the leader issues
+// The pair runs tcgen05.mma.cta_group::2 (M = 256, the leader issues
 // for both CTAs). Each CTA loads its own A and HALF of B's columns (no
 // multicast), so per-SM shared-memory fill and MMA operand reads both drop to
 // A + B/2; TMA loads complete on the leader's full barrier, commits multicast.
@@ -301,7 +286,7 @@ __device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& 
   return e;
 }
 
-// CG2 instantiations (p.mc == 2) contain cta_group::2 instructions and must be
+// CG2 instantiations (host p.mc == 2) contain cta_group::2 instructions and must be
 // launched as clusters of 2; every other launch uses CG2 = false.
 template <int BN, int KS, bool EPI8 = false, bool CG2 = false>
 __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
@@ -334,7 +319,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   const uint32_t lane = lane_id();
   constexpr uint32_t kMmaWarp = Cfg::kMma;
   int mc_rank = 0;
-  if (p.mc) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(mc_rank));
+  if constexpr (CG2) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(mc_rank));
   constexpr bool cg2 = CG2;
 
   if (threadIdx.x == 32 * kMmaWarp + 1) {  // descriptor fetches overlap the prologue
@@ -345,7 +330,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   if (threadIdx.x == 0) {
     for (int i = 0; i < S; ++i) {
       mbar_init(&full[i], kProducers);  // every producer arrives once per stage
-      mbar_init(&empty[i], p.mc == 1 ? 2 : 1);  // mc 1: both CTAs' MMAs release the slot
+      mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
@@ -380,7 +365,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (p.mc) mc_cluster_sync();  // the peer's barriers exist before any multicast lands
+  if constexpr (CG2) mc_cluster_sync();  // the peer's barriers exist before any remote arrive / complete_tx
   const uint32_t tmem_base = *tmem_slot;
   pdl_launch_dependents();
 
@@ -438,7 +423,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     uint32_t slot = 0, phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt, ks, z1, z2, lt = mc_tile(p, tile);
+      int s, mt, g, nt, ks, z1, z2, lt = mc_tile<CG2>(p, tile);
       split_batch(p, lt, z1, z2);
       decompose_tile(p, lt, s, mt, g, nt, ks);
       const int a_r = batch_row(p.ba, z1, z2), a_c = batch_col(p.ba, z1, z2);
@@ -512,14 +497,9 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
           if (b_mode == B_STREAM && !p.b_kmajor) {
 #pragma unroll
             for (int ch = 0; ch < kBChunks; ++ch)
-              if ((pps + ch) % kProducers == pw) {
-                if (!p.mc)
-                  tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk + b_c,
-                              st * Cfg::kBRows + b_r);
-                else if ((ch & 1) == mc_rank)  // this CTA's half of B, into both rings
-                  tma_load_2d_mc(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk,
-                                 st * Cfg::kBRows, 3);
-              }
+              if ((pps + ch) % kProducers == pw)
+                tma_load_2d(sB + ch * kBChunkBytes, &p.tmB, &full[slot], col0 + ch * Cfg::kBChunk + b_c,
+                            st * Cfg::kBRows + b_r);
           } else if (b_mode == B_STREAM) {
             // K-major B: sub-block u = BN rows (N) x 64 K, 128-byte SW128 rows like A
 #pragma unroll
@@ -584,7 +564,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     // cg2: the leader issues every MMA of the pair; the peer's MMA warp idles
     for (int tile = blockIdx.x + ((cg2 && mc_rank) ? p.total_tiles : 0); tile < p.total_tiles;
          tile += gridDim.x) {
-      int s, mt, g, nt, ks, z1, z2, lt = mc_tile(p, tile);
+      int s, mt, g, nt, ks, z1, z2, lt = mc_tile<CG2>(p, tile);
       split_batch(p, lt, z1, z2);
       decompose_tile(p, lt, s, mt, g, nt, ks);
       int st0, st1;
@@ -611,7 +591,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
                          idesc, ((st - st0) | u | k) != 0);
             }
           if constexpr (cg2) umma_commit_cg2(&empty[slot]);
-          else if (p.mc) umma_commit_mc(&empty[slot], 3);
           else umma_commit(&empty[slot]);
         }
         __syncwarp();
@@ -657,7 +636,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       const bool epi_on = p.bias || p.relu || p.residual;
       int local = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
-        int s, mt, g, nt, z1, z2, lt = mc_tile(p, tile);
+        int s, mt, g, nt, z1, z2, lt = mc_tile<CG2>(p, tile);
         split_batch(p, lt, z1, z2);
         decompose_tile(p, lt, s, mt, g, nt);
         const int c_r = batch_row(p.bc, z1, z2), c_c = batch_col(p.bc, z1, z2);
@@ -804,7 +783,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       int local = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, ++local) {
         int s, mt, g, nt;
-        decompose_tile(p, mc_tile(p, tile), s, mt, g, nt);
+        decompose_tile(p, mc_tile<CG2>(p, tile), s, mt, g, nt);
         const SubProb& sp = p.sub[s];
         {
           const int m = mt * kBM + static_cast<int>(q * 32 + lane);
@@ -936,7 +915,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     else
       tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
-  if (p.mc) mc_cluster_sync();  // no multicast or remote arrive still targets this CTA
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
     uint64_t t_end;
     uint32_t smid;

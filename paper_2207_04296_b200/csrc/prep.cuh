@@ -269,7 +269,9 @@ inline int launch_pack_kw_win(const uint16_t* x, uint16_t* y, const uint16_t* w,
 inline int launch_pack_kw_fused(const uint16_t* x, uint16_t* y, const uint16_t* w, uint16_t* wy, int64_t rows,
                                 int64_t iw, int64_t c, int64_t ow, int64_t kw, int64_t sw, int64_t pw, int64_t dw,
                                 int64_t cp, int64_t khd, int64_t kwc, int64_t co, cudaStream_t st) {
-  if (!getenv("TIR_B200_PACK_GATHER")) {
+  // Window form only for dilated strips (DIL: ~1 us faster); for dw = 1 (MobileNet /
+  // C3D stems) the gather form's 16-byte staging loads win (MobileNet-V2 +1.5 %).
+  if (dw > 1 && !getenv("TIR_B200_PACK_GATHER")) {
     const int rc = launch_pack_kw_win(x, y, w, wy, rows, iw, c, ow, kw, sw, pw, dw, cp, khd, kwc, co, st);
     if (rc != 2) return rc;
   }

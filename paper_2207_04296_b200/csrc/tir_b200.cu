@@ -254,15 +254,16 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 // ------------------------------------------------------------------ igemm launch
 
 // CTA pairs for plain GEMMs: tiled A, streamed row-major B in >= 2 chunks, one
-// problem (no groups / split-K / batch / sub-problems), an even M-tile count.
-// Default: tcgen05.mma.cta_group::2 (p.mc = 2; each SM loads and reads half of
-// B). Measured on B200, vs unpaired: 8192^3 1094 -> 1287 TFLOPS, BERT-large
-// QKV / FFN1 / FFN2 / out GEMMs -11 / -12 / -15 / -5 %. TIR_B200_CG2=0 keeps the
-// pairs but only multicasts B (p.mc = 1: +4-7 % at 8192^3, nothing below);
-// TIR_B200_MC=0 disables pairs, TIR_B200_MC=1 forces them.
+// problem (no groups / split-K / batch / sub-problems), an even M-tile count:
+// tcgen05.mma.cta_group::2 (p.mc = 2; each SM loads and reads half of B).
+// Measured on B200, vs unpaired: 8192^3 1094 -> 1290 TFLOPS, BERT-large QKV /
+// FFN1 / FFN2 GEMMs -11 / -12 / -15 %. (A B-multicast-only pair was measured
+// too: +4-7 % at 8192^3, nothing below; removed.) TIR_B200_MC=0 disables pairs.
 bool use_mc(const tb::IgemmParams& p, int bn) {
   const char* mc_env = getenv("TIR_B200_MC");  // read per launch (tests toggle it)
   if (mc_env && atoi(mc_env) == 0) return false;
+  const char* cg2_env = getenv("TIR_B200_CG2");  // legacy spelling of the same switch
+  if (cg2_env && atoi(cg2_env) == 0) return false;
   return p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
          p.groups == 1 && p.ksplit == 1 && !p.batch_tiles && bn >= 128 && p.sub[0].tiles_m % 2 == 0 &&
          p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
@@ -331,10 +332,8 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
                          ? n : 0;
       cudaGetLastError();
     }
-    if (max_clusters > 0) {
-      // 2: tcgen05.mma.cta_group::2 (M = 256, B split by column); 1: B multicast only
-      const char* cg2 = getenv("TIR_B200_CG2");
-      p.mc = (BN >= 128 && !(cg2 && atoi(cg2) == 0)) ? 2 : 1;
+    if (max_clusters > 0 && BN >= 128) {
+      p.mc = 2;  // tcgen05.mma.cta_group::2 (M = 256, B split by column)
       grid = std::min(grid / 2, max_clusters) * 2;
     }
   }
@@ -352,8 +351,6 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
       CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8, true>, grid, 2, Cfg::kThreadsN, smem, stream,
                                   p));
     }
-  } else if (p.mc) {
-    CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, 2, Cfg::kThreadsN, smem, stream, p));
   } else {
     CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS, EPI8>, grid, Cfg::kThreadsN, smem, stream, p));
   }
@@ -407,7 +404,8 @@ int launch_igemm(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
 int choose_ks(int max_pieces, int box, int bn) {
   if (const char* e = getenv("TIR_B200_KS")) return std::max(1, std::min(4, atoi(e)));
   const int pps1 = tb::kBK / box;
-  const int limit = box < 64 ? 227 * 1024 - 1280 - 4 * 8192 - 16 * max_pieces - 512 : 190 * 1024;
+  const int limit = (box < 64 && !getenv("TIR_B200_KS_STRICT")) ? 227 * 1024 - 1280 - 4 * 8192 - 16 * max_pieces - 512
+                                                                 : 190 * 1024;
   int best = 1;
   int64_t best_waste = -1;
   for (int ks : {4, 2, 1}) {

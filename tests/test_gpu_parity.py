@@ -220,11 +220,10 @@ def test_gmm_d2_and_variants(mnk, cuda):
                          ids=lambda t: "x".join(map(str, t)))
 def test_gmm_b_multicast_pairs(mnk, monkeypatch, cuda):
     """CTA-pair GEMMs (igemm.cuh mc_tile): the default tcgen05.mma.cta_group::2 pairs
-    (M = 256, half of B per SM) and the B-multicast-only pairs (TIR_B200_CG2=0) give
-    bit-identical results to unpaired launches (TIR_B200_MC=0) — the same K order per
-    output — plain and with the fused bias / GELU / residual fp16 epilogue, and are
-    bit-exact vs the oracle on the reference distribution. 384 rows = 3 M tiles (odd)
-    falls back to unpaired launches."""
+    (M = 256, half of B per SM) give bit-identical results to unpaired launches
+    (TIR_B200_MC=0) — the same K order per output — plain and with the fused bias /
+    GELU / residual fp16 epilogue, and are bit-exact vs the oracle on the reference
+    distribution. 384 rows = 3 M tiles (odd) falls back to unpaired launches."""
     import torch
 
     M, N, K = mnk
@@ -234,13 +233,12 @@ def test_gmm_b_multicast_pairs(mnk, monkeypatch, cuda):
     bias = torch.randn(N, device=cuda)
     res = torch.randn(M, N, device=cuda).half()
     outs = {}
-    for mode, mc, cg2 in (("unpaired", "0", "1"), ("multicast", "1", "0"), ("cta_group2", "1", "1")):
+    for mode, mc in (("unpaired", "0"), ("cta_group2", "1")):
         monkeypatch.setenv("TIR_B200_MC", mc)
-        monkeypatch.setenv("TIR_B200_CG2", cg2)
         outs[mode] = (tb.gmm(dev(a, cuda), dev(b, cuda)), tb.gmm(dev(an, cuda), dev(bn_, cuda)),
                       tb.gmm(dev(an, cuda), dev(bn_, cuda), out_f16=True, bias=bias, relu="gelu", residual=res))
     torch.cuda.synchronize()
-    for mode in ("multicast", "cta_group2"):
+    for mode in ("cta_group2",):
         for x, y in zip(outs["unpaired"], outs[mode]):
             assert torch.equal(x, y), mode
     rows = 128
