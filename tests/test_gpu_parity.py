@@ -218,7 +218,7 @@ def test_gmm_d2_and_variants(mnk, cuda):
 
 @pytest.mark.parametrize("mnk", [(1024, 1024, 1024), (2048, 512, 2048), (384, 256, 256), (4096, 1024, 4096)],
                          ids=lambda t: "x".join(map(str, t)))
-def test_gmm_b_multicast_pairs(mnk, monkeypatch, cuda):
+def test_gmm_cta_pairs(mnk, monkeypatch, cuda):
     """CTA-pair GEMMs (igemm.cuh mc_tile): the default tcgen05.mma.cta_group::2 pairs
     (M = 256, half of B per SM) give bit-identical results to unpaired launches
     (TIR_B200_MC=0) — the same K order per output — plain and with the fused bias /
@@ -235,8 +235,11 @@ def test_gmm_b_multicast_pairs(mnk, monkeypatch, cuda):
     outs = {}
     for mode, mc in (("unpaired", "0"), ("cta_group2", "1")):
         monkeypatch.setenv("TIR_B200_MC", mc)
+        acc = torch.from_numpy(O.normal_f16((M, N), 5).astype(np.float32)).to(cuda)
+        tb.gmm(dev(an, cuda), dev(bn_, cuda), acc, accumulate=True)
         outs[mode] = (tb.gmm(dev(a, cuda), dev(b, cuda)), tb.gmm(dev(an, cuda), dev(bn_, cuda)),
-                      tb.gmm(dev(an, cuda), dev(bn_, cuda), out_f16=True, bias=bias, relu="gelu", residual=res))
+                      tb.gmm(dev(an, cuda), dev(bn_, cuda), out_f16=True, bias=bias, relu="gelu", residual=res),
+                      tb.gmm(dev(an, cuda), dev(bn_, cuda), out_f16=True, bias=bias), acc)
     torch.cuda.synchronize()
     for mode in ("cta_group2",):
         for x, y in zip(outs["unpaired"], outs[mode]):
