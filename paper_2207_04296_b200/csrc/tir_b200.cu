@@ -259,7 +259,7 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 // Measured on B200, vs unpaired: 8192^3 1094 -> 1290 TFLOPS, BERT-large QKV /
 // FFN1 / FFN2 GEMMs -11 / -12 / -15 %. (A B-multicast-only pair was measured
 // too: +4-7 % at 8192^3, nothing below; removed.) TIR_B200_MC=0 disables pairs.
-bool use_mc(const tb::IgemmParams& p, int bn) {
+bool use_pairs(const tb::IgemmParams& p, int bn) {
   const char* mc_env = getenv("TIR_B200_MC");  // read per launch (tests toggle it)
   if (mc_env && atoi(mc_env) == 0) return false;
   const char* cg2_env = getenv("TIR_B200_CG2");  // legacy spelling of the same switch
@@ -313,7 +313,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
                                 static_cast<int>(smem)));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
   p.mc = 0;
-  if (use_mc(p, BN) && grid >= 2) {
+  if (use_pairs(p, BN) && grid >= 2) {
     static int max_clusters = -1;  // per instantiation: same smem / block for every launch that gets here
     if (max_clusters < 0) {
       cudaLaunchConfig_t cfg{};
