@@ -100,6 +100,19 @@ const char* tir_b200_last_error(void);
 int64_t tir_b200_launch_count(void);
 void tir_b200_reset_launch_count(void);
 
+/* Relayout scratch is one grow-only device buffer per (device, stream); a
+ * CUDA graph captured over a CI % 8 != 0 conv keeps pointing at it, so buffers
+ * are never freed implicitly. Call this only when no captured graph or
+ * in-flight launch still uses them (it synchronises every device it touched). */
+int tir_b200_release_workspaces(void);
+
+/* Planner switches (csrc/options.h): tile shape, pipeline depth,
+ * epilogue flavour — never the result. Initialised once from TIR_B200_<NAME>
+ * environment variables; these calls change them at run time for the whole
+ * process. Returns TIR_B200_ERR_VALUE for an unknown name. */
+int tir_b200_set_option(const char* name, int value);
+int tir_b200_get_option(const char* name, int* value);
+
 /* Output extents (OD, OH, OW) for a descriptor; validates it. */
 int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]);
 
@@ -158,10 +171,6 @@ int tir_b200_layernorm(const uint16_t* X, uint16_t* Y, const float* gamma, const
 /* Y[r, :] = softmax(scale * X[r, :]) (fp32 internally), cols <= 8192. */
 int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols, float scale,
                      void* stream);
-
-/* Y[c, r] = X[r, col0 + c] (fp16; rows % 8 == 0, ld_in / ld_out / col0 multiples of 8). */
-int tir_b200_transpose(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t ld_in, int64_t col0,
-                       int64_t cols, int64_t ld_out, void* stream);
 
 /* ---- batched GMM (attention: per-(sequence, head) problems over strided views) ----
  * Problem z = z1 * z2n + z2 (0 <= z1 < z1n, 0 <= z2 < z2n) computes

@@ -16,10 +16,11 @@ from .api import (  # noqa: F401
     conv_host,
     gmm,
     gmm_batched,
-    transpose,
     gmm_host,
     launch_count,
     lib,
     reset_launch_count,
+    set_option,
+    get_option,
     useful_macs,
 )

@@ -183,6 +183,10 @@ OpMatch match_contraction(const tir::PrimFunc& f, const std::string& block) {
   Stmt realize = find_realize(f, block);
   const tir::Block& B = *realize->block;
   if (B.annotations.count("tensorized")) mismatch("block '" + block + "' is already tensorized");
+  // A guarded block (a `where` predicate, e.g. from a padded split) writes only
+  // part of its domain; the whole-op kernels write every output element.
+  if (realize->predicate && !tir::is_true(realize->predicate))
+    mismatch("block '" + block + "' has a predicate; whole-op kernels cannot honour it");
   std::map<std::string, IterInfo> iters;
   for (const auto& iv : B.iter_vars) {
     IterInfo info;
@@ -338,6 +342,7 @@ OpMatch match_contraction(const tir::PrimFunc& f, const std::string& block) {
     transposed = tr;
     if (tr) {
       if (co_ != 1 && O[i] != 1) mismatch("transposed index must be (o + p - k*d) / s");
+      if (cr == 0 && K[i] != 1) mismatch("input index ignores an iterator");
       S[i] = s;
       D[i] = cr == 0 ? 1 : -cr;
       P[i] = c0;

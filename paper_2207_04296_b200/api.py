@@ -140,7 +140,6 @@ def lib() -> ctypes.CDLL:
         L.tir_b200_avgpool_global.argtypes = [vp, vp, i64, i64, i64, vp]
         L.tir_b200_layernorm.argtypes = [vp, vp, vp, vp, i64, i64, ctypes.c_float, vp]
         L.tir_b200_softmax.argtypes = [vp, vp, i64, i64, ctypes.c_float, vp]
-        L.tir_b200_transpose.argtypes = [vp, vp, i64, i64, i64, i64, i64, vp]
         L.tir_b200_gmm_batched.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, i64, i64,
                                            ctypes.POINTER(BatchDesc), i32, ctypes.POINTER(Epilogue), vp]
         L.tir_b200_conv_host_f32.argtypes = [ctypes.POINTER(ConvDesc), vp, vp, vp, i32]
@@ -159,6 +158,17 @@ def launch_count() -> int:
 
 def reset_launch_count() -> None:
     lib().tir_b200_reset_launch_count()
+
+
+def set_option(name: str, value: int) -> None:
+    """Planner switch (csrc/options.h): tile shape / pipeline / epilogue flavour, never results."""
+    _check(lib().tir_b200_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int(0)
+    _check(lib().tir_b200_get_option(name.encode(), ctypes.byref(v)))
+    return v.value
 
 
 # ---------------------------------------------------------------- device tensors
@@ -317,18 +327,6 @@ def softmax(X, scale: float = 1.0, Y=None, *, stream=None):
         Y = torch.empty_like(X)
     _need(Y, torch.float16, (rows, cols), "Y")
     _check(lib().tir_b200_softmax(_ptr(X), _ptr(Y), rows, cols, scale, _stream(stream)))
-    return Y
-
-
-def transpose(X, col0: int, cols: int, Y=None, *, stream=None):
-    """Y [cols, rows] = X[:, col0:col0+cols]^T for a row-major fp16 X [rows, ld]."""
-    torch = _torch()
-    rows, ld = X.shape
-    _need(X, torch.float16, (rows, ld), "X")
-    if Y is None:
-        Y = torch.empty((cols, rows), dtype=torch.float16, device=X.device)
-    _need(Y, torch.float16, (cols, Y.shape[1]), "Y")
-    _check(lib().tir_b200_transpose(_ptr(X), _ptr(Y), rows, ld, col0, cols, Y.shape[1], _stream(stream)))
     return Y
 
 

@@ -53,46 +53,31 @@ struct alignas(64) HaloParams {
   const uint16_t* residual;  // fused epilogue: fp16 residual in Y's layout (store_mode 0 only)
   int32_t store_mode;         // 0: direct register stores, 1: TMA store, 2: TMA reduce-add (Y += )
   int32_t nacc;               // TMEM accumulator buffers (MMA runs nacc-1 tiles ahead)
-  int32_t linear;             // 1: tile = 128 consecutive virtual pixels of the OH x Wv image
-                              //    (tiles_h tiles per image, tiles_w = 1; direct-store epilogue)
   int32_t stage_bytes;        // TMA-store staging buffer bytes (one of two)
   void* Y;
   const float* Yin;
   unsigned long long* trace;
 };
 
-// TAPN ("tap-packed N", 3x3 stride-1 undilated, BN = 64): one MMA covers the
-// KW horizontal taps of a kernel row at once, N = KW * BN = 192 columns
-// D_tx[v, co] = sum_ci X[v + ty*Wv, ci] W[ty, tx, ci, co] (the resident weight
-// rows of taps (ty, 0..KW-1) are three consecutive 64-row blocks = the three
-// N chunks of one MN-major descriptor, LBO = one tap). The epilogue forms
-// Y[m] = D_0[m] + D_1[m + 1] + D_2[m + 2] with lane shuffles (plus a 96-float
-// exchange across TMEM lane quadrants). Per output tile that is 12 MMAs reading
-// A once per kernel row instead of 36 reading it once per tap: the MMA's
-// shared-memory operand traffic drops from 216 KB to 120 KB per tile, the
-// limiter of the N = 64 headline conv (tools/mma_rate.cu: N = 64 runs at 48
-// instead of 32 cycles per MMA because A and B saturate the SMEM read port).
-template <int BN, bool TAPN = false>
+template <int BN>
 struct HaloCfg {
   static constexpr int kBChunk = BN < 64 ? BN : 64;
   static constexpr int kBRowBytes = kBChunk * 2;
   static constexpr uint32_t kBLayout = kBRowBytes == 128 ? 2u : kBRowBytes == 64 ? 4u : 6u;
-  static constexpr int kN = TAPN ? 3 * BN : BN;            // MMA N (accumulator columns per tile)
+  static constexpr int kN = BN;  // MMA N (accumulator columns per tile)
   static constexpr uint32_t kIdesc = idesc_f16_f32(128, kN, 0, 1);
   static constexpr int kNacc = (4 * kN <= 512) ? 4 : 2;   // accumulator buffers
   static constexpr int kTmemCols = (kNacc * kN <= 32) ? 32 : (kNacc * kN <= 64) ? 64
                                    : (kNacc * kN <= 128) ? 128 : (kNacc * kN <= 256) ? 256 : 512;
-  static constexpr int kXchBytes = TAPN ? 2 * 2 * 4 * 96 * 4 : 0;  // [parity][half][quadrant][96] fp32
   static size_t smem_bytes(int stages, int slab_rows, int b_rows, int stage_bytes) {
     return 1024 + static_cast<size_t>(stages) * slab_rows * 128 +
-           static_cast<size_t>(b_rows) * BN * 2 + 2 * static_cast<size_t>(stage_bytes) + kXchBytes + 256;
+           static_cast<size_t>(b_rows) * BN * 2 + 2 * static_cast<size_t>(stage_bytes) + 256;
   }
 };
 
-template <int BN, int KH, int KW, bool TAPN = false>  // KH = KW = 0: runtime kernel extents
+template <int BN, int KH, int KW>  // KH = KW = 0: runtime kernel extents
 __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid_constant__ HaloParams p) {
-  using Cfg = HaloCfg<BN, TAPN>;
-  static_assert(!TAPN || (KH == 3 && KW == 3 && BN == 64), "tap-packed N: 3x3, BN = 64");
+  using Cfg = HaloCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -101,8 +86,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   uint8_t* sA0 = smem;
   uint8_t* sB = smem + static_cast<size_t>(S) * slab_bytes;
   uint8_t* epi = sB + static_cast<size_t>(p.b_rows) * BN * 2;  // 1024-aligned (host)
-  float* xch = reinterpret_cast<float*>(epi + 2 * p.stage_bytes);  // TAPN quadrant exchange
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + 2 * p.stage_bytes + Cfg::kXchBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + 2 * p.stage_bytes);
   uint64_t* empty = full + S;
   uint64_t* tfull = empty + S;           // [kNacc]
   uint64_t* tempty = tfull + Cfg::kNacc;  // [kNacc]
@@ -122,7 +106,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     }
     for (int i = 0; i < Cfg::kNacc; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], (p.store_mode && !TAPN) ? 128 : 256);  // modes 1-3 use warps 0-3; mode 0, TAPN all 8
+      mbar_init(&tempty[i], p.store_mode ? 128 : 256);  // TMA-store modes use warps 0-3; mode 0 all 8
     }
     mbar_init(bfull, 1);
     fence_barrier_init();
@@ -166,8 +150,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         int n, th, tw, g, nt;
         decompose(tile, n, th, tw, g, nt);
-        // linear: the slab starts at the first output row the 128-pixel window touches
-        const int y0 = (p.linear ? (th * 128) / p.Wv : th * p.R) - p.pad_h;
+        const int y0 = th * p.R - p.pad_h;
         const int x0 = tw * p.Wt - p.pad_w;
         for (int cb = 0; cb < p.cblocks; ++cb, ++it) {
           mbar_wait(&empty[slot], phase ^ 1);
@@ -200,8 +183,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   } else if (warp == 9) {
     // ------------------------------------------------------------ MMA issuer
     const uint64_t a0 = smem_desc(smem_u32(sA0), 16, 1024, 2);
-    // TAPN: the N chunks of one MMA are the KW taps of a kernel row: LBO = one tap's rows
-    const uint64_t b0 = smem_desc(smem_u32(sB), TAPN ? p.cig * Cfg::kBRowBytes : p.b_rows * Cfg::kBRowBytes,
+    const uint64_t b0 = smem_desc(smem_u32(sB), p.b_rows * Cfg::kBRowBytes,
                                   8 * Cfg::kBRowBytes, Cfg::kBLayout);
     const uint32_t slab16 = slab_bytes >> 4;
     // descriptor start-address units (16 B): one virtual pixel row = 128 B = 8
@@ -210,7 +192,6 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     const int cig_b = (p.cig * Cfg::kBRowBytes) >> 4;  // weight rows of one tap
     constexpr uint32_t kBk16 = (16 * Cfg::kBRowBytes) >> 4;
     const int taps = p.kh * p.kw;
-    const int it_dummy = 0;
     if (static_cast<int>(blockIdx.x) < p.total_tiles) {
       mbar_wait(bfull, 0);
       tc_fence_after();
@@ -239,15 +220,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       if (nslot == static_cast<uint32_t>(S)) { nslot = 0; nphase ^= 1; }
       if (last_cb && ++nacc == static_cast<uint32_t>(Cfg::kNacc)) { nacc = 0; nacc_phase ^= 1; }
       if (trace && lane == 0 && i < 128) trace[256 + 2 * i] = clock64();
-      uint32_t lin_off = 0;  // linear tiles: window start within the slab's first row (16-B units)
-      if (p.linear) {
-        const int tile = static_cast<int>(blockIdx.x) + (i / p.cblocks) * static_cast<int>(gridDim.x);
-        int n, th, tw, g, nt;
-        decompose(tile, n, th, tw, g, nt);
-        const int v0 = th * 128;
-        lin_off = static_cast<uint32_t>(v0 - (v0 / p.Wv) * p.Wv) * 8u;
-      }
-      const uint64_t a_slab = a0 + slot * slab16 + lin_off;
+      const uint64_t a_slab = a0 + slot * slab16;
       const uint64_t b_cb = b0 + ((static_cast<uint32_t>(cb * 64) * Cfg::kBRowBytes) >> 4);
       auto issue_tap = [&](int ty, int tx, int t) {
         const uint64_t a = a_slab + static_cast<uint32_t>(ty * wv_dil + tx * dil8);
@@ -257,28 +230,6 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
           umma_f16(tmem_d, a + 2u * k, b + k * kBk16, Cfg::kIdesc, (cb | t | k) != 0);
       };
       const bool leader = elect_one();
-      if constexpr (TAPN) {
-        // kernel row ty: A shifted by ty rows of the virtual image, B = taps (ty, 0..2)
-        auto issue_row = [&](int ty) {
-          const uint64_t a = a_slab + static_cast<uint32_t>(ty * wv_dil);
-          const uint64_t b = b_cb + static_cast<uint32_t>(ty * KW * cig_b);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16(tmem_d, a + 2u * k, b + k * kBk16, Cfg::kIdesc, (cb | ty | k) != 0);
-        };
-        if (leader) {
-#pragma unroll
-          for (int ty = 0; ty < KH - 1; ++ty) issue_row(ty);
-        }
-        __syncwarp();
-        if (i + 1 < nstage) wait_stage(i + 1, nslot, nphase, nacc, nacc_phase);
-        if (leader) {
-          issue_row(KH - 1);
-          umma_commit(&empty[slot]);
-          if (last_cb) umma_commit(&tfull[acc]);
-        }
-        __syncwarp();
-      } else {
       if constexpr (KH > 0) {
         if (leader) {
 #pragma unroll
@@ -298,206 +249,8 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
         if (last_cb) umma_commit(&tfull[acc]);
       }
       __syncwarp();
-      }
       if (trace && lane == 0 && i < 128) trace[256 + 2 * i + 1] = clock64();
       slot = nslot; phase = nphase; acc = nacc; acc_phase = nacc_phase;
-    }
-    (void)it_dummy;
-  } else if (TAPN) {
-    // ------------------------------------------------------------ epilogue, tap-packed N (TMA store)
-    // Warp w: TMEM lane quadrant q = w % 4, output column half hc = w / 4 (32 of
-    // the 64 channels). Thread = virtual pixel m; Y[m] = D_0[m] + D_1[m+1] +
-    // D_2[m+2] (this fixed order), the +1 / +2 rows from the next lanes by
-    // shuffle and, for the last lanes of a quadrant, from the next quadrant's
-    // warp through shared memory. Then bias / residual / activation, the
-    // [R][Wt][32] staging box of this half and one TMA store per tile and half.
-    if (warp < 8) {
-      pdl_wait();  // Y may still be read by the preceding kernel
-      const uint32_t q = warp & 3, hc = warp >> 2;
-      const int m = static_cast<int>(q * 32 + lane);
-      const int ry = m / p.Wv, cx = m - ry * p.Wv;
-      const bool mine = ry < p.R && cx < p.Wt;
-      const int line = ry * p.Wt + cx;
-      const int line_bytes = p.out_f16 ? 64 : 128;
-      const uint32_t bar_id = 3 + hc;  // named barrier of this half's 4 warps
-      const bool issuer = (q == 0 && lane == 0);
-      uint8_t* buf = epi + hc * p.stage_bytes;
-      uint32_t acc = 0, acc_phase = 0, par = 0;
-      const bool epi_on = p.bias || p.relu || p.residual;
-      int local = 0;
-      const bool tr = trace && threadIdx.x == 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x, par ^= 1, ++local) {
-        unsigned long long* tt = (tr && local < 8) ? trace + 1536 + 8 * local : nullptr;
-        if (tt) tt[0] = clock64();
-        int n, th, tw, g, nt;
-        decompose(tile, n, th, tw, g, nt);
-        const int c0 = static_cast<int>(hc) * 32;
-        const int64_t colb = static_cast<int64_t>(g) * p.cog + nt * BN + c0;
-        const float bias_l = p.bias ? __ldg(p.bias + colb + lane) : 0.0f;
-        const uint16_t* res_row = nullptr;
-        if (p.residual && mine) {
-          const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
-          if (oy < p.oh && ox < p.ow)
-            res_row = p.residual + ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + colb;
-        }
-        uint4 rp[4];
-        if (res_row && (reinterpret_cast<uintptr_t>(res_row) & 15) == 0) {
-#pragma unroll
-          for (int i = 0; i < 4; ++i) rp[i] = __ldg(reinterpret_cast<const uint4*>(res_row) + i);
-        }
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-        if (tt) tt[1] = clock64();
-        uint32_t v0[32], v1[32], v2[32];
-        const uint32_t base = tmem_base + ((q * 32u) << 16) + acc * Cfg::kN + c0;
-        tmem_ld_32x32b_x32(base, v0);
-        tmem_ld_32x32b_x32(base + BN, v1);
-        tmem_ld_32x32b_x32(base + 2 * BN, v2);
-        tmem_ld_wait();
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);  // accumulator drained into registers
-        if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
-        // publish this quadrant's first rows for the quadrant above: D_1 row 0, D_2 rows 0-1
-        const uint32_t xo = smem_u32(xch + ((par * 2 + hc) * 4 + q) * 96);
-        if (lane == 0) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            sts_f32(xo + 4 * i, __uint_as_float(v1[i]));
-            sts_f32(xo + 4 * (32 + i), __uint_as_float(v2[i]));
-          }
-        } else if (lane == 1) {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) sts_f32(xo + 4 * (64 + i), __uint_as_float(v2[i]));
-        }
-        if (tt) tt[2] = clock64();
-        named_bar_sync(bar_id, 128);
-        if (tt) tt[3] = clock64();
-        // q = 3 reads its own slot: rows >= 128 are never valid outputs
-        const uint32_t xn = smem_u32(xch + ((par * 2 + hc) * 4 + (q < 3 ? q + 1 : q)) * 96);
-        const uint32_t xn2 = xn + 4 * (32 + 32 * (lane & 1));  // lanes 30 / 31: D_2 rows 0 / 1
-        float y[32];
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float a1 = __shfl_down_sync(0xffffffffu, __uint_as_float(v1[i]), 1);
-          const float a2 = __shfl_down_sync(0xffffffffu, __uint_as_float(v2[i]), 2);
-          const float n1 = lds_f32(xn + 4 * i);   // same address in every lane: broadcast
-          const float n2 = lds_f32(xn2 + 4 * i);
-          y[i] = (__uint_as_float(v0[i]) + (lane == 31 ? n1 : a1)) + (lane >= 30 ? n2 : a2);
-        }
-        if (epi_on) {
-          const int lim = p.cog - (nt * BN + c0);
-          if (p.bias) {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) y[i] += __shfl_sync(0xffffffffu, bias_l, i);
-          }
-          if (res_row) {
-            if (lim >= 32 && (reinterpret_cast<uintptr_t>(res_row) & 15) == 0) {
-#pragma unroll
-              for (int i = 0; i < 4; ++i) {
-                const __half2* hv = reinterpret_cast<const __half2*>(&rp[i]);
-#pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  const float2 f = __half22float2(hv[j]);
-                  y[8 * i + 2 * j] += f.x;
-                  y[8 * i + 2 * j + 1] += f.y;
-                }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 32; ++i)
-                if (i < lim)
-                  y[i] += __half2float(__ushort_as_half(__ldg(reinterpret_cast<const unsigned short*>(res_row) + i)));
-            }
-          }
-          epi_act_n<32>(y, p.relu);
-        }
-        // staging buffer of this half: free once the previous tile's store has read it
-        if (tt) tt[4] = clock64();
-        if (issuer) tma_store_wait_read<0>();
-        named_bar_sync(bar_id, 128);
-        if (tt) tt[5] = clock64();
-        if (mine) {
-          uint8_t* dst = buf + line * line_bytes;
-          if (p.out_f16) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint4 u;
-              __half2 h0 = __floats2half2_rn(y[8 * c], y[8 * c + 1]);
-              __half2 h1 = __floats2half2_rn(y[8 * c + 2], y[8 * c + 3]);
-              __half2 h2 = __floats2half2_rn(y[8 * c + 4], y[8 * c + 5]);
-              __half2 h3 = __floats2half2_rn(y[8 * c + 6], y[8 * c + 7]);
-              u.x = *reinterpret_cast<uint32_t*>(&h0);
-              u.y = *reinterpret_cast<uint32_t*>(&h1);
-              u.z = *reinterpret_cast<uint32_t*>(&h2);
-              u.w = *reinterpret_cast<uint32_t*>(&h3);
-              *reinterpret_cast<uint4*>(dst + ((c ^ ((line >> 1) & 3)) << 4)) = u;  // SW64
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 8; ++c)
-              *reinterpret_cast<uint4*>(dst + ((c ^ (line & 7)) << 4)) =
-                  make_uint4(__float_as_uint(y[4 * c]), __float_as_uint(y[4 * c + 1]),
-                             __float_as_uint(y[4 * c + 2]), __float_as_uint(y[4 * c + 3]));  // SW128
-          }
-        }
-        fence_proxy_async_smem();
-        named_bar_sync(bar_id, 128);
-        if (issuer) {
-          const int col = static_cast<int>(colb);
-          if (p.store_mode == 2)
-            tma_reduce_add_4d(&p.tmY, buf, col, tw * p.Wt, th * p.R, n);
-          else
-            tma_store_4d(&p.tmY, buf, col, tw * p.Wt, th * p.R, n);
-          tma_store_commit();
-        }
-        if (tt) tt[6] = clock64();
-      }
-      if (issuer) tma_store_wait_all<0>();
-    }
-  } else if (p.store_mode == 3) {
-    // ------------------------------------------------------------ epilogue, 256-bit direct stores
-    // Warps 0-3: tcgen05.ld 32x32b (thread = virtual pixel) straight to
-    // st.global.v8.f32 (32 B per thread, 32 full sectors per instruction); no
-    // shared-memory traffic (the kernel's limiter is SMEM bandwidth).
-    if (warp < 4) {
-      pdl_wait();
-      const uint32_t q = warp;
-      const int m = static_cast<int>(q * 32 + lane);
-      const int ry = m / p.Wv, cx = m - ry * p.Wv;
-      uint32_t acc = 0, acc_phase = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-        int n, th, tw, g, nt;
-        decompose(tile, n, th, tw, g, nt);
-        const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
-        const bool ok = ry < p.R && cx < p.Wt && oy < p.oh && ox < p.ow;
-        float* yrow = reinterpret_cast<float*>(p.Y) +
-                      ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + g * p.cog + nt * BN;
-        mbar_wait(&tfull[acc], acc_phase);
-        tc_fence_after();
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 32) {
-          uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + acc * BN + c0, r);
-          tmem_ld_wait();
-          if (ok) {
-#pragma unroll
-            for (int v = 0; v < 4; ++v)
-              asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(yrow + c0 + 8 * v),
-                           "r"(r[8 * v]), "r"(r[8 * v + 1]), "r"(r[8 * v + 2]), "r"(r[8 * v + 3]),
-                           "r"(r[8 * v + 4]), "r"(r[8 * v + 5]), "r"(r[8 * v + 6]), "r"(r[8 * v + 7])
-                           : "memory");
-          }
-        }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
-          acc = 0;
-          acc_phase ^= 1;
-        }
-      }
     }
   } else if (p.store_mode) {
     // ------------------------------------------------------------ epilogue, TMA store
@@ -644,17 +397,9 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       int n, th, tw, g, nt;
       decompose(tile, n, th, tw, g, nt);
       auto row_offset = [&](int m) -> int64_t {
-        int oy, ox;
-        if (p.linear) {  // virtual pixel v of the OH x Wv image; columns >= OW are discarded
-          const int v = th * 128 + m;
-          oy = v / p.Wv;
-          ox = v - oy * p.Wv;
-        } else {
-          const int ry = m / p.Wv, cx = m - ry * p.Wv;
-          if (ry >= p.R || cx >= p.Wt) return -1;
-          oy = th * p.R + ry;
-          ox = tw * p.Wt + cx;
-        }
+        const int ry = m / p.Wv, cx = m - ry * p.Wv;
+        if (ry >= p.R || cx >= p.Wt) return -1;
+        const int oy = th * p.R + ry, ox = tw * p.Wt + cx;
         if (oy >= p.oh || ox >= p.ow) return -1;
         return ((static_cast<int64_t>(n) * p.oh + oy) * p.ow + ox) * p.co + g * p.cog + nt * BN;
       };

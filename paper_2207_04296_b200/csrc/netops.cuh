@@ -316,36 +316,3 @@ __global__ void __launch_bounds__(256) layernorm_warp_kernel(const uint16_t* __r
 
 }  // namespace tb
 
-namespace tb {
-
-// Y[c, r] = X[r, col0 + c] for r < rows, c < cols (fp16): 64x64 tiles through
-// shared memory, 16-byte global accesses on both sides. Used to lay K out as
-// the [d, tokens] B operand of the batched attention GEMM.
-__global__ void transpose_kernel(const uint16_t* __restrict__ X, uint16_t* __restrict__ Y, int rows,
-                                 int ld_in, int col0, int cols, int ld_out) {
-  __shared__ uint16_t t[64][64 + 8];
-  const int r0 = blockIdx.y * 64, c0 = blockIdx.x * 64;
-  // load: 64 rows x 64 cols = 512 16-byte vectors, 256 threads x 2
-  for (int v = threadIdx.x; v < 512; v += blockDim.x) {
-    const int rr = v / 8, cv = v % 8;
-    const int r = r0 + rr, c = c0 + cv * 8;
-    uint4 u = make_uint4(0, 0, 0, 0);
-    if (r < rows && c < cols) u = __ldg(reinterpret_cast<const uint4*>(X + static_cast<int64_t>(r) * ld_in + col0 + c));
-    const uint16_t* h = reinterpret_cast<const uint16_t*>(&u);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) t[rr][cv * 8 + j] = h[j];
-  }
-  __syncthreads();
-  for (int v = threadIdx.x; v < 512; v += blockDim.x) {
-    const int cc = v / 8, rv = v % 8;
-    const int c = c0 + cc, r = r0 + rv * 8;
-    if (c >= cols || r >= rows) continue;
-    uint4 u;
-    uint16_t* h = reinterpret_cast<uint16_t*>(&u);
-#pragma unroll
-    for (int j = 0; j < 8; ++j) h[j] = t[rv * 8 + j][cc];
-    *reinterpret_cast<uint4*>(Y + static_cast<int64_t>(c) * ld_out + r) = u;
-  }
-}
-
-}  // namespace tb

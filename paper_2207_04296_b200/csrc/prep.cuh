@@ -16,6 +16,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include "options.h"
+
 namespace tb {
 
 __global__ void pad_channels_kernel(const uint16_t* __restrict__ x, uint16_t* __restrict__ y,
@@ -271,7 +273,7 @@ inline int launch_pack_kw_fused(const uint16_t* x, uint16_t* y, const uint16_t* 
                                 int64_t cp, int64_t khd, int64_t kwc, int64_t co, cudaStream_t st) {
   // Window form only for dilated strips (DIL: ~1 us faster); for dw = 1 (MobileNet /
   // C3D stems) the gather form's 16-byte staging loads win (MobileNet-V2 +1.5 %).
-  if (dw > 1 && !getenv("TIR_B200_PACK_GATHER")) {
+  if (dw > 1 && !options().pack_gather) {
     const int rc = launch_pack_kw_win(x, y, w, wy, rows, iw, c, ow, kw, sw, pw, dw, cp, khd, kwc, co, st);
     if (rc != 2) return rc;
   }

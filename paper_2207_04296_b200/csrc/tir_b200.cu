@@ -21,9 +21,9 @@
 #include "../../include/tir_b200.h"
 #include "dep.cuh"
 #include "halo.cuh"
-#include "halo2.cuh"
 #include "igemm.cuh"
 #include "netops.cuh"
+#include "options.h"
 #include "prep.cuh"
 
 namespace {
@@ -180,29 +180,46 @@ bool is_depthwise(const Geo& g) { return g.g == g.ci && g.ci == g.co && !g.trans
 
 // ------------------------------------------------------------------ workspace
 
+// Relayout scratch (channel pad, (kw, c) / (kh, kw, c) packing), one buffer per
+// (device, stream): kernels on one stream are ordered, so calls that share a
+// stream may share its buffer; two streams never do. Grow-only and never freed
+// while the process runs: a CUDA graph captured over a relayout keeps the raw
+// pointer, so a later, larger request gets a NEW buffer and the old one stays
+// valid (retired, not freed). tir_b200_release_workspaces() frees everything
+// once the caller knows no graph or in-flight launch references it.
 struct Workspace {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
   void* ptr = nullptr;
   size_t bytes = 0;
-  int dev = -1;
 };
-thread_local Workspace t_ws;
+std::mutex g_ws_mu;
+std::vector<Workspace> g_ws;       // live buffers, one per (device, stream)
+std::vector<void*> g_ws_retired;   // outgrown buffers (may still be referenced by graphs)
 
-int workspace(size_t bytes, void** out) {
+int workspace(size_t bytes, cudaStream_t stream, void** out) {
   int dev = 0;
   CUDA_TRY(cudaGetDevice(&dev));
-  if (t_ws.dev != dev || t_ws.bytes < bytes) {
-    if (t_ws.ptr) {
-      int cur = dev;
-      cudaSetDevice(t_ws.dev);
-      cudaFree(t_ws.ptr);
-      cudaSetDevice(cur);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  for (Workspace& w : g_ws) {
+    if (w.dev != dev || w.stream != stream) continue;
+    if (w.bytes < bytes) {
+      void* p = nullptr;
+      CUDA_TRY(cudaMalloc(&p, bytes));
+      g_ws_retired.push_back(w.ptr);
+      w.ptr = p;
+      w.bytes = bytes;
     }
-    t_ws = Workspace{};
-    CUDA_TRY(cudaMalloc(&t_ws.ptr, bytes));
-    t_ws.bytes = bytes;
-    t_ws.dev = dev;
+    *out = w.ptr;
+    return TIR_B200_OK;
   }
-  *out = t_ws.ptr;
+  Workspace w;
+  w.dev = dev;
+  w.stream = stream;
+  w.bytes = bytes;
+  CUDA_TRY(cudaMalloc(&w.ptr, bytes));
+  g_ws.push_back(w);
+  *out = w.ptr;
   return TIR_B200_OK;
 }
 
@@ -215,7 +232,7 @@ int workspace(size_t bytes, void** out) {
 template <typename Params>
 cudaError_t launch_pdl(void (*kernel)(Params), int grid, int block, size_t smem, cudaStream_t stream,
                        const Params& p) {
-  static const bool no_pdl = getenv("TIR_B200_NO_PDL") != nullptr;
+  const bool no_pdl = tb::options().no_pdl != 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -233,7 +250,7 @@ cudaError_t launch_pdl(void (*kernel)(Params), int grid, int block, size_t smem,
 template <typename Params>
 cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, int block, size_t smem,
                                cudaStream_t stream, const Params& p) {
-  static const bool no_pdl = getenv("TIR_B200_NO_PDL") != nullptr;
+  const bool no_pdl = tb::options().no_pdl != 0;
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(block);
@@ -260,10 +277,7 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 // FFN1 / FFN2 GEMMs -11 / -12 / -15 %. (A B-multicast-only pair was measured
 // too: +4-7 % at 8192^3, nothing below; removed.) TIR_B200_MC=0 disables pairs.
 bool use_pairs(const tb::IgemmParams& p, int bn) {
-  const char* mc_env = getenv("TIR_B200_MC");  // read per launch (tests toggle it)
-  if (mc_env && atoi(mc_env) == 0) return false;
-  const char* cg2_env = getenv("TIR_B200_CG2");  // legacy spelling of the same switch
-  if (cg2_env && atoi(cg2_env) == 0) return false;
+  if (!tb::options().mc) return false;
   return p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
          p.groups == 1 && p.ksplit == 1 && !p.batch_tiles && bn >= 128 && p.sub[0].tiles_m % 2 == 0 &&
          p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
@@ -282,7 +296,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   const int nbias = p.groups * p.cog;
   p.bias_floats = (p.bias && p.store_mode && !p.batch_tiles && nst_all * KS * tb::kBK <= 256 && nbias <= 4096 &&
                    p.cog % 32 == 0 &&
-                   (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0 && !getenv("TIR_B200_NO_SMEM_BIAS"))
+                   (reinterpret_cast<uintptr_t>(p.bias) & 15) == 0 && !tb::options().no_smem_bias)
                       ? (nbias + 3) / 4 * 4 : 0;
   // the staged bias must not cost the ring its second stage
   if (p.bias_floats && di.smem_optin - 1280 - table - p.bias_floats * 4 - Cfg::kEpiBytes <
@@ -341,8 +355,8 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes / 2));
     smem = Cfg::smem_bytes(p.stages, 0, p.total_pieces, p.bias_floats, true);
   }
-  if (const char* e = getenv("TIR_B200_MAX_CTAS"))
-    grid = p.mc ? std::max(2, std::min(grid, atoi(e) / 2 * 2)) : std::max(1, std::min(grid, atoi(e)));
+  if (const int e = tb::options().max_ctas)
+    grid = p.mc ? std::max(2, std::min(grid, e / 2 * 2)) : std::max(1, std::min(grid, e));
   p.trace = g_trace;
   if (p.mc == 2) {
     if constexpr (BN >= 128) {
@@ -364,7 +378,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
 // (IgemmCfg EPI8). Measured: ResNet-50 forward -8%, MobileNet-V2 -13%; the
 // paper's fp32-output convs keep 4 producers (GRP / DIL lose 5-8% with 3).
 bool use_epi8(const tb::IgemmParams& p, int bn, int ks) {
-  if (const char* e = getenv("TIR_B200_EPI8")) return atoi(e) != 0;
+  if (tb::options().epi8 >= 0) return tb::options().epi8 != 0;
   int nst = 0;
   for (int i = 0; i < p.num_sub; ++i) nst = std::max(nst, p.sub[i].num_stages);
   const bool fused = p.out_f16 || p.bias || p.relu || p.residual;
@@ -405,9 +419,9 @@ int launch_igemm(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
 // two stages may use everything but the 4-warp staging (DIL: one 256-deep stage
 // per tile instead of two, 36.9 -> 34.9 us).
 int choose_ks(int max_pieces, int box, int bn) {
-  if (const char* e = getenv("TIR_B200_KS")) return std::max(1, std::min(4, atoi(e)));
+  if (const int e = tb::options().ks) return std::max(1, std::min(4, e));
   const int pps1 = tb::kBK / box;
-  const int limit = (box < 64 && !getenv("TIR_B200_KS_STRICT")) ? 227 * 1024 - 1280 - 4 * 8192 - 16 * max_pieces - 512
+  const int limit = (box < 64 && !tb::options().ks_strict) ? 227 * 1024 - 1280 - 4 * 8192 - 16 * max_pieces - 512
                                                                  : 190 * 1024;
   int best = 1;
   int64_t best_waste = -1;
@@ -471,9 +485,10 @@ Epi make_epi(const tir_b200_epilogue* e) {
 int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64_t rows, int accumulate,
                     int out_f16) {
   p.store_mode = 0;
-  if (getenv("TIR_B200_NO_TMA_STORE")) return TIR_B200_OK;
-  // Reduce-add cannot apply bias/ReLU after the add: accumulate + epilogue stays generic.
-  if (accumulate && (p.bias || p.relu)) return TIR_B200_OK;
+  if (tb::options().no_tma_store) return TIR_B200_OK;
+  // Reduce-add cannot apply the epilogue after the add (the ABI order is
+  // (Yin + acc) + bias + residual, then the activation): accumulate + epilogue stays generic.
+  if (accumulate && (p.bias || p.relu || p.residual)) return TIR_B200_OK;
   if (bn < 32 || !(p.groups == 1 || p.cog % 32 == 0) || (accumulate && Yin != Y)) return TIR_B200_OK;
   if ((reinterpret_cast<uintptr_t>(Y) & 15) || (p.ldy * (out_f16 ? 2 : 4)) % 16) return TIR_B200_OK;
   int rc = encode_y(p, Y, rows, out_f16, bn);
@@ -488,7 +503,7 @@ int pick_store_mode(tb::IgemmParams& p, int bn, void* Y, const float* Yin, int64
 // with waves = ceil(tiles / SMs). A narrower tile must be >= 20% cheaper to
 // win: the model ignores the extra L2 traffic of re-reading A per N tile.
 int choose_bn(int64_t cols, int64_t m_tiles, int64_t groups, int64_t k_steps, int sms) {
-  if (const char* e = getenv("TIR_B200_BN")) return atoi(e);
+  if (const int e = tb::options().bn) return e;
   int bn_max = 16;
   while (bn_max < cols && bn_max < 256) bn_max *= 2;
   int best = bn_max;
@@ -546,7 +561,7 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
 // so Y is first zeroed (or seeded with Yin when accumulating). Sums of the
 // reference distribution are exact in any order, so parity is unchanged.
 int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int sms) {
-  if (const char* e = getenv("TIR_B200_KSPLIT")) return std::max(1, atoi(e));
+  if (const int e = tb::options().ksplit) return std::max(1, e);
   if (out_f16 || p.bias || p.relu || p.residual || out_tiles * 2 > sms) return 1;  // epilogue needs the full sum
   int nst_min = 1 << 30;
   for (int i = 0; i < p.num_sub; ++i) nst_min = std::min(nst_min, p.sub[i].num_stages);
@@ -786,48 +801,25 @@ int pick_box(int64_t cig) {
 
 constexpr int kNotEligible = -100;  // halo path declines; caller uses im2col
 
-template <int BN, int KH, int KW, bool TAPN = false>
+template <int BN, int KH, int KW>
 int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
-  using Cfg = tb::HaloCfg<BN, TAPN>;
+  using Cfg = tb::HaloCfg<BN>;
   const DeviceInfo di = device_info();
   const int keys = p.groups * p.tiles_n;
   if (keys > di.sms) return kNotEligible;
   if (BN > 64 && p.b_rows * Cfg::kBRowBytes >= (1 << 18)) return kNotEligible;
-  const int fixed = 1024 + 256 + p.b_rows * BN * 2 + 2 * p.stage_bytes + Cfg::kXchBytes;
+  const int fixed = 1024 + 256 + p.b_rows * BN * 2 + 2 * p.stage_bytes;
   const int slab = p.slab_rows * 128;
   const int stages = std::min(4, (di.smem_optin - fixed) / slab);
   if (stages < 2) return kNotEligible;
   p.stages = stages;
   const size_t smem = Cfg::smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW, TAPN>,
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   int grid = std::min(p.total_tiles, di.sms / keys * keys);
-  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(1, std::min(grid, atoi(e)));
+  if (const int e = tb::options().max_ctas) grid = std::max(1, std::min(grid, e));
   p.trace = g_trace;
-  CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW, TAPN>, grid, tb::kHaloThreads, smem, stream, p));
-  ++g_launches;
-  return TIR_B200_OK;
-}
-
-// The CTA-pair variant (halo2.cuh): 64 output channels, one group, TMA-store epilogue.
-int launch_halo2(tb::HaloParams& p, const uint16_t* W, cudaStream_t stream) {
-  const DeviceInfo di = device_info();
-  // weights: this CTA's 32-column half, boxes of b_box_rows rows (64-byte rows, SW64)
-  int rc = encode_2d(&p.tmW, W, p.b_rows, p.co, tb::kPairBHalf, p.b_box_rows);
-  if (rc) return rc;
-  const int fixed = 1024 + 256 + p.b_rows * tb::kPairBHalf * 2 + 2 * p.stage_bytes;
-  const int slab = p.slab_rows * 128;
-  const int stages = std::min(4, (di.smem_optin - fixed) / slab);
-  if (stages < 2) return kNotEligible;
-  p.stages = stages;
-  const size_t smem = tb::halo2_smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
-  const int pairs = (p.total_tiles + 1) / 2;
-  int grid = 2 * std::min(pairs, di.sms / 2);
-  if (const char* e = getenv("TIR_B200_MAX_CTAS")) grid = std::max(2, std::min(grid, atoi(e) / 2 * 2));
-  p.trace = g_trace;
-  CUDA_TRY(launch_pdl_cluster(tb::conv_halo2_kernel, grid, 2, tb::kHaloThreads, smem, stream, p));
+  CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW>, grid, tb::kHaloThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
 }
@@ -836,7 +828,7 @@ int launch_halo2(tb::HaloParams& p, const uint16_t* W, cudaStream_t stream) {
 // for shapes outside its envelope.
 int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
                    int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
-  if (getenv("TIR_B200_NO_HALO")) return kNotEligible;
+  if (tb::options().no_halo) return kNotEligible;
   if (g.transposed || g.in[0] != 1 || g.k[0] != 1 || g.p[0] != 0) return kNotEligible;
   if (g.s[1] != 1 || g.s[2] != 1 || g.d[1] != g.d[2]) return kNotEligible;
   const int64_t cig = g.ci / g.g, cog = g.co / g.g;
@@ -856,31 +848,8 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   const int64_t Wv = Wt + (KW - 1) * d;
   int64_t HR = R + (KH - 1) * d;
   const int64_t max_off = (KH - 1) * d * Wv + (KW - 1) * d;
-  const DeviceInfo di0 = device_info();
-  // Linear tiles (full-width rows only): a tile is 128 consecutive virtual pixels
-  // of the OH x Wv virtual output image instead of R whole rows. Waste drops from
-  // (128 - R*OW)/128 to (Wv - OW)/Wv and the tile count no longer rounds up per
-  // row block (C2D 56x56: 448 -> 416 tiles, i.e. 3 instead of 4 per SM). The slab
-  // covers every row a window starting anywhere in a row can touch.
-  // Opt-in (TIR_B200_HALO_LINEAR=1): measured on B200 the bigger slab and the
-  // direct-store epilogue add more SMEM/LSU traffic per tile than the saved wave
-  // costs (C2D paper shape 9.7 -> 10.9 us), because the kernel is SMEM-bound.
-  bool linear = false;
-  if (Wt == OW && getenv("TIR_B200_HALO_LINEAR")) {
-    const int64_t rect = g.n * ((OH + R - 1) / R);
-    const int64_t lin = g.n * ((OH * Wv + 127) / 128);
-    const int64_t lin_hr = (Wv - 1 + 127) / Wv + 1 + (KH - 1) * d;
-    const int64_t sms = di0.sms;
-    const int64_t lin_rows = std::max(lin_hr * Wv, Wv - 1 + max_off + 128);
-    if ((lin + sms - 1) / sms < (rect + sms - 1) / sms && lin_hr <= 256 && lin_rows <= tb::kHaloMaxRows) {
-      linear = true;
-      R = 1;
-      HR = lin_hr;
-    }
-  }
   if (Wv > 256 || HR > 256) return kNotEligible;
   int64_t slab_rows = std::max(HR * Wv, max_off + 128);
-  if (linear) slab_rows = std::max(slab_rows, Wv - 1 + max_off + 128);
   slab_rows = (slab_rows + 7) / 8 * 8;
   if (slab_rows > tb::kHaloMaxRows) return kNotEligible;
   const int64_t taps = KH * KW;
@@ -905,8 +874,7 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   p.Wv = static_cast<int32_t>(Wv);
   p.HR = static_cast<int32_t>(HR);
   p.tiles_w = static_cast<int32_t>((OW + Wt - 1) / Wt);
-  p.tiles_h = static_cast<int32_t>(linear ? (OH * Wv + 127) / 128 : (OH + R - 1) / R);
-  p.linear = linear ? 1 : 0;
+  p.tiles_h = static_cast<int32_t>((OH + R - 1) / R);
   p.cblocks = static_cast<int32_t>(cig / 64);
   p.b_rows = static_cast<int32_t>(taps * cig);
   p.slab_rows = static_cast<int32_t>(slab_rows);
@@ -954,13 +922,8 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   // updated in place (reduce-add). Otherwise direct register stores.
   p.store_mode = 0;
   p.stage_bytes = 0;
-  if (linear) {
-    // direct register stores (generic mode 0): a linear tile is not a TMA box
-  } else if (getenv("TIR_B200_STORE256") && !epi.on() && bn >= 32 && cog % 32 == 0 && !accumulate && !out_f16 &&
-      g.co % 8 == 0 && (reinterpret_cast<uintptr_t>(Y) & 31) == 0) {
-    p.store_mode = 3;
-  } else if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || (Yin == Y && !epi.on())) &&
-      !getenv("TIR_B200_NO_TMA_STORE")) {
+  if (bn >= 32 && (g.g == 1 || cog % 32 == 0) && (!accumulate || (Yin == Y && !epi.on())) &&
+      !tb::options().no_tma_store) {
     const Driver* drv = driver();
     const int esz = out_f16 ? 2 : 4;
     cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.co), static_cast<cuuint64_t>(OW),
@@ -980,20 +943,6 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
     }
   }
   const bool k3 = KH == 3 && KW == 3;
-  // CTA pairs (halo2.cuh): M = 256 per MMA, half the weights per SM.
-  if (bn == 64 && g.co == 64 && g.g == 1 && p.tiles_n == 1 && !linear && (p.store_mode == 1 || p.store_mode == 2) &&
-      getenv("TIR_B200_PAIR")) {
-    const int rc = launch_halo2(p, W, stream);
-    if (rc != kNotEligible) return rc;
-  }
-  // Tap-packed N (halo.cuh): 3x3 undilated, 64-column tiles, TMA-store epilogue.
-  // Opt-in (TIR_B200_TAPN=1): measured on B200 it cuts the MMA time per C2D tile
-  // from ~2500 to ~1150 cycles, but reading the 3x wider accumulator out of TMEM
-  // (~1000 cycles per tile) plus the row-shift adds make the epilogue the
-  // limiter (13.6 vs 9.6 us for the paper shape).
-  if (k3 && d == 1 && bn == 64 && !linear && (p.store_mode == 1 || p.store_mode == 2) &&
-      getenv("TIR_B200_TAPN"))
-    return launch_halo_bn<64, 3, 3, true>(p, stream);
   switch (bn) {
     case 16: return k3 ? launch_halo_bn<16, 3, 3>(p, stream) : launch_halo_bn<16, 0, 0>(p, stream);
     case 32: return k3 ? launch_halo_bn<32, 3, 3>(p, stream) : launch_halo_bn<32, 0, 0>(p, stream);
@@ -1026,13 +975,13 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   const int64_t kw_cp = g.k[2] * cig <= 8 ? 8 : g.k[2] * cig <= 16 ? 16 : g.k[2] * cig <= 32 ? 32 : 64;
   const bool hw_small = g.out[1] * hw_cp * 2 <= 3 * g.in[1] * kw_cp;  // per output column, per image row block
   if (cig % 8 && g.g == 1 && !g.transposed && g.k[1] > 1 && g.k[1] * g.k[2] * cig <= 256 &&
-      (getenv("TIR_B200_PACK_HW") || (hw_small && !getenv("TIR_B200_NO_PACK_HW")))) {
+      (tb::options().pack_hw == 1 || (hw_small && tb::options().pack_hw != 0))) {
     const int64_t cp = hw_cp;
     const int64_t rows = g.n * g.in[0] * g.out[1];
     const size_t xbytes = static_cast<size_t>(rows * g.out[2] * cp * 2);
     const size_t wbytes = static_cast<size_t>(g.k[0] * cp * g.co * 2);
     void* ws = nullptr;
-    int rc = workspace(xbytes + wbytes + 512, &ws);
+    int rc = workspace(xbytes + wbytes + 512, stream, &ws);
     if (rc) return rc;
     uint16_t* Xp = static_cast<uint16_t*>(ws);
     uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
@@ -1060,7 +1009,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   // channel dim ((kw, c) packing, prep.cuh) so each im2col piece carries
   // KW*CI real channels instead of CI padded to 8. Bit-exact relayout.
   if (cig % 8 && g.g == 1 && !g.transposed && g.k[2] > 1 && g.k[2] * cig <= 64 &&
-      !getenv("TIR_B200_NO_PACK_KW")) {
+      tb::options().pack_kw) {
     const int64_t kwc = g.k[2] * cig;
     const int64_t cp = kwc <= 8 ? 8 : kwc <= 16 ? 16 : kwc <= 32 ? 32 : 64;
     const int64_t rows = g.n * g.in[0] * g.in[1];
@@ -1068,7 +1017,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     const size_t xbytes = static_cast<size_t>(rows * g.out[2] * cp * 2);
     const size_t wbytes = static_cast<size_t>(khd * cp * g.co * 2);
     void* ws = nullptr;
-    int rc = workspace(xbytes + wbytes + 512, &ws);
+    int rc = workspace(xbytes + wbytes + 512, stream, &ws);
     if (rc) return rc;
     uint16_t* Xp = static_cast<uint16_t*>(ws);
     uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
@@ -1105,7 +1054,7 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     const size_t xbytes = static_cast<size_t>(pix * cip * 2);
     const size_t wbytes = static_cast<size_t>(taps * cip * g.co * 2);
     void* ws = nullptr;
-    int rc = workspace(xbytes + wbytes + 256, &ws);
+    int rc = workspace(xbytes + wbytes + 256, stream, &ws);
     if (rc) return rc;
     uint16_t* Xp = static_cast<uint16_t*>(ws);
     uint16_t* Wp = reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + (xbytes + 255) / 256 * 256);
@@ -1355,13 +1304,13 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
   const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0) &&
                        (!accumulate || reinterpret_cast<uintptr_t>(Yin) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(X) % 16 == 0);
-  if (!getenv("TIR_B200_DEP_SIMPLE") && aligned && g.ci % 8 == 0 && g.ci >= 32 && g.k[1] == 3 && g.k[2] == 3 &&
+  if (!tb::options().dep_simple && aligned && g.ci % 8 == 0 && g.ci >= 32 && g.k[1] == 3 && g.k[2] == 3 &&
       g.d[1] == 1 && g.d[2] == 1 && g.s[1] == g.s[2] && (g.s[1] == 1 || g.s[1] == 2)) {
     const int64_t ow = g.out[2];
-    const char* tc_env = getenv("TIR_B200_DEP_TC");  // tile-shape override (tuning)
-    if (g.s[1] == 1 && tc_env && atoi(tc_env) == 16)
+    const int tc = tb::options().dep_tc;  // tile-width override (tuning)
+    if (g.s[1] == 1 && tc == 16)
       return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
-    if (g.s[1] == 1 && tc_env && atoi(tc_env) == 8)
+    if (g.s[1] == 1 && tc == 8)
       return launch_dep_tile<3, 1, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
     if (g.s[1] == 1) {
       if (ow >= 24) return launch_dep_tile<3, 1, 4, 2, 8, 32>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
@@ -1486,6 +1435,45 @@ const char* tir_b200_last_error(void) { return g_err.c_str(); }
 int64_t tir_b200_launch_count(void) { return g_launches; }
 void tir_b200_reset_launch_count(void) { g_launches = 0; }
 
+int tir_b200_release_workspaces(void) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  int cur = 0;
+  CUDA_TRY(cudaGetDevice(&cur));
+  CUDA_TRY(cudaDeviceSynchronize());
+  for (void* p : g_ws_retired) cudaFree(p);
+  for (Workspace& w : g_ws) {
+    cudaSetDevice(w.dev);
+    cudaDeviceSynchronize();
+    cudaFree(w.ptr);
+  }
+  cudaSetDevice(cur);
+  g_ws_retired.clear();
+  g_ws.clear();
+  return TIR_B200_OK;
+}
+
+int tir_b200_set_option(const char* name, int value) {
+  int n = 0;
+  const tb::OptionEntry* t = tb::option_table(&n);
+  for (int i = 0; name && i < n; ++i)
+    if (!strcmp(name, t[i].name)) {
+      tb::options().*(t[i].field) = value;
+      return TIR_B200_OK;
+    }
+  return set_err(TIR_B200_ERR_VALUE, "unknown option '%s'", name ? name : "(null)");
+}
+
+int tir_b200_get_option(const char* name, int* value) {
+  int n = 0;
+  const tb::OptionEntry* t = tb::option_table(&n);
+  for (int i = 0; name && value && i < n; ++i)
+    if (!strcmp(name, t[i].name)) {
+      *value = tb::options().*(t[i].field);
+      return TIR_B200_OK;
+    }
+  return set_err(TIR_B200_ERR_VALUE, "unknown option '%s'", name ? name : "(null)");
+}
+
 int tir_b200_conv_out_shape(const tir_b200_conv_desc* desc, int64_t out_dhw[3]) {
   Geo g{};
   int rc = make_geo(desc, &g);
@@ -1557,7 +1545,7 @@ int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const 
   // the GPU overlap across chunks. Only for convs that need no shared library
   // workspace (CI / G a multiple of 8: no relayout kernels).
   const int64_t cig = g.ci / g.g;
-  const int nch = (cig % 8 == 0 && g.n >= 2 && !getenv("TIR_B200_NO_HOST_PIPELINE"))
+  const int nch = (cig % 8 == 0 && g.n >= 2 && tb::options().host_pipeline)
                       ? static_cast<int>(std::min<int64_t>(g.n, 8)) : 1;
   const int64_t x_img = xe / g.n, y_img = ye / g.n;
   CUDA_TRY(cudaEventRecord(t_host.ev[0], st));  // weights uploaded
@@ -1745,21 +1733,6 @@ int tir_b200_softmax(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t cols,
   if (vpt == 1) tb::softmax_kernel<1><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
   else if (vpt == 2) tb::softmax_kernel<2><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
   else tb::softmax_kernel<4><<<g, threads, 0, st>>>(X, Y, (int)cols, scale);
-  CUDA_TRY(cudaGetLastError());
-  ++g_launches;
-  return TIR_B200_OK;
-}
-
-int tir_b200_transpose(const uint16_t* X, uint16_t* Y, int64_t rows, int64_t ld_in, int64_t col0, int64_t cols,
-                       int64_t ld_out, void* stream) {
-  int rc = check_vec(X, Y, 8);
-  if (rc) return rc;
-  if (rows <= 0 || cols <= 0 || rows % 8 || ld_in % 8 || ld_out % 8 || col0 % 8 || col0 + cols > ld_in ||
-      rows > ld_out || rows >= (1ll << 31) || cols >= (1ll << 31))
-    return set_err(TIR_B200_ERR_VALUE, "transpose: bad geometry");
-  dim3 grid(static_cast<unsigned>((cols + 63) / 64), static_cast<unsigned>((rows + 63) / 64));
-  tb::transpose_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(X, Y, (int)rows, (int)ld_in, (int)col0,
-                                                                          (int)cols, (int)ld_out);
   CUDA_TRY(cudaGetLastError());
   ++g_launches;
   return TIR_B200_OK;

@@ -39,3 +39,21 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.fail("GPU test run without a visible CUDA device")
     return torch.device("cuda:0")
+
+
+@pytest.fixture
+def option():
+    """Sets libtir_b200 planner switches (tir_b200_set_option) for one test and
+    restores them afterwards."""
+    import paper_2207_04296_b200 as tb
+
+    saved = {}
+
+    def set_(name, value):
+        if name not in saved:
+            saved[name] = tb.get_option(name)
+        tb.set_option(name, value)
+
+    yield set_
+    for k, v in saved.items():
+        tb.set_option(k, v)

@@ -135,12 +135,6 @@ def test_gmm_residual_gelu(cuda):
         tb.gmm(a, b, relu="swish")
 
 
-def test_transpose_exact(cuda):
-    x = torch.randn(136, 72, device=cuda).half()
-    y = tb.transpose(x, 8, 64)
-    assert torch.equal(y, x[:, 8:72].t().contiguous())
-
-
 @pytest.mark.parametrize("n_dim", [64, 256])
 def test_gmm_batched_strided_heads(n_dim, cuda):
     """Per-(sequence, head) problems over strided views, as in attention."""

@@ -218,10 +218,10 @@ def test_gmm_d2_and_variants(mnk, cuda):
 
 @pytest.mark.parametrize("mnk", [(1024, 1024, 1024), (2048, 512, 2048), (384, 256, 256), (4096, 1024, 4096)],
                          ids=lambda t: "x".join(map(str, t)))
-def test_gmm_cta_pairs(mnk, monkeypatch, cuda):
+def test_gmm_cta_pairs(mnk, option, cuda):
     """CTA-pair GEMMs (igemm.cuh mc_tile): the default tcgen05.mma.cta_group::2 pairs
     (M = 256, half of B per SM) give bit-identical results to unpaired launches
-    (TIR_B200_MC=0) — the same K order per output — plain and with the fused bias /
+    (option mc = 0) — the same K order per output — plain and with the fused bias /
     GELU / residual fp16 epilogue, and are bit-exact vs the oracle on the reference
     distribution. 384 rows = 3 M tiles (odd) falls back to unpaired launches."""
     import torch
@@ -233,8 +233,8 @@ def test_gmm_cta_pairs(mnk, monkeypatch, cuda):
     bias = torch.randn(N, device=cuda)
     res = torch.randn(M, N, device=cuda).half()
     outs = {}
-    for mode, mc in (("unpaired", "0"), ("cta_group2", "1")):
-        monkeypatch.setenv("TIR_B200_MC", mc)
+    for mode, mc in (("unpaired", 0), ("cta_group2", 1)):
+        option("mc", mc)
         acc = torch.from_numpy(O.normal_f16((M, N), 5).astype(np.float32)).to(cuda)
         tb.gmm(dev(an, cuda), dev(bn_, cuda), acc, accumulate=True)
         outs[mode] = (tb.gmm(dev(a, cuda), dev(b, cuda)), tb.gmm(dev(an, cuda), dev(bn_, cuda)),
@@ -300,14 +300,15 @@ def test_native_kernels_actually_launch(cuda):
     assert tb.launch_count() == 2
 
 
-@pytest.mark.parametrize("variant", ["TIR_B200_TAPN", "TIR_B200_HALO_LINEAR", "TIR_B200_PAIR", "TIR_B200_STORE256"])
-def test_opt_in_halo_variants_exact(variant, monkeypatch, cuda):
-    """The measured-and-rejected halo variants (tap-packed N, linear tiles) stay
-    correct: bit-exact on the reference distribution, with bias + ReLU and fp16
-    output, at the paper's C2D shape (sampled images) and a small wide shape."""
-    monkeypatch.setenv(variant, "1")
+@pytest.mark.parametrize("switch", [("no_halo", 1), ("no_tma_store", 1), ("epi8", 1), ("ks", 1), ("mc", 0),
+                                    ("no_pdl", 1)], ids=lambda t: f"{t[0]}={t[1]}")
+def test_planner_switches_exact(switch, option, cuda):
+    """Planner switches (tir_b200_set_option) change tiling / epilogue flavour,
+    never results: bit-exact on the reference distribution, with bias + ReLU and
+    fp16 output, at the paper's C2D shape (sampled images) and a small wide shape."""
     import torch
 
+    option(*switch)
     for spec in (tb.PAPER_SHAPES["C2D"], tb.Conv("C2D", n=2, in_dhw=(1, 5, 140), ci=64, co=64, k=(1, 3, 3),
                                                   p=(0, 1, 1))):
         x = O.reference_tensor(spec.x_shape(), 21)
@@ -319,15 +320,15 @@ def test_opt_in_halo_variants_exact(variant, monkeypatch, cuda):
         one = ospec(spec.with_(n=1))
         for img in (0, spec.n - 1):
             want = O.conv(one, x[img:img + 1], w, threads=8)
-            assert O.tensors_bitwise_equal(got[img:img + 1], want), (variant, img)
+            assert O.tensors_bitwise_equal(got[img:img + 1], want), (switch, img)
             ref16 = np.maximum(want + bias, 0).astype(np.float16).astype(np.float32)
-            assert np.array_equal(fused[img:img + 1], ref16), (variant, img)
+            assert np.array_equal(fused[img:img + 1], ref16), (switch, img)
 
 
 @pytest.mark.parametrize("name", ["DIL", "C3D"])
-def test_opt_in_pack_hw_exact(name, monkeypatch, cuda):
-    """The opt-in (kh, kw, c) relayout (TIR_B200_PACK_HW) stays bit-exact."""
-    monkeypatch.setenv("TIR_B200_PACK_HW", "1")
+def test_opt_in_pack_hw_exact(name, option, cuda):
+    """The opt-in (kh, kw, c) relayout (pack_hw = 1) stays bit-exact."""
+    option("pack_hw", 1)
     spec = SMALL[name]
     x = O.reference_tensor(spec.x_shape(), 31)
     w = O.reference_tensor(spec.w_shape(), 32)

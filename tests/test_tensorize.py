@@ -160,6 +160,12 @@ def test_rejects_non_contractions_and_partial_nests():
     with pytest.raises(api.TirError) as e:
         tensorize(unguarded, "conv")
     assert e.value.kind == "DescMismatch"
+    # a guarded (predicated) contraction writes part of its domain: never whole-op
+    guarded = G.gmm_source(16, 16, 16).replace(") {\n            init", ") if i < 8 {\n            init")
+    assert " if i < 8 {" in guarded
+    with pytest.raises(api.TirError) as e:
+        tensorize(guarded, "gemm")
+    assert e.value.kind == "DescMismatch" and "predicate" in e.value.message
 
 
 def test_tensorized_block_keeps_init_and_regions():
