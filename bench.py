@@ -65,6 +65,25 @@ def dist_env():
     return world, rank, local
 
 
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def spawn_ranks(n: int) -> None:
+    """`bench.py --gpus N` outside torchrun: re-execute this command under
+    torch.distributed.run with N ranks (one process per GPU, 127.0.0.1
+    rendezvous), exactly as the driver launches it; returns only on failure."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
 def init_dist(world, backend):
     import torch.distributed as dist
 
@@ -136,7 +155,18 @@ class ClockSampler:
 EXTRA_SHAPES = {
     "GMM8K": (8192, 8192, 8192),                     # peak demo
     "C2D_L3": dict(op="C2D", n=16, in_dhw=(1, 14, 14), ci=256, co=256, k=(1, 3, 3), p=(0, 1, 1)),
+    "FLOOR": (128, 64, 64),                          # one-CTA GEMM: the per-launch floor
 }
+# The MobileNet-V2 depthwise layers (BASELINE configs[3]), all 3x3 p1, N = 16.
+DEP_SHAPES = {"DEP": (112, 32, 1), "DEP_112c96s2": (112, 96, 2), "DEP_56c144s1": (56, 144, 1),
+              "DEP_56c144s2": (56, 144, 2), "DEP_28c192s1": (28, 192, 1), "DEP_28c192s2": (28, 192, 2),
+              "DEP_14c384s1": (14, 384, 1), "DEP_14c576s1": (14, 576, 1), "DEP_14c576s2": (14, 576, 2),
+              "DEP_7c960s1": (7, 960, 1)}
+for _n, (_hw, _c, _s) in DEP_SHAPES.items():
+    if _n != "DEP":
+        EXTRA_SHAPES[_n] = dict(op="DEP", n=16, in_dhw=(1, _hw, _hw), ci=_c, co=_c, k=(1, 3, 3), s=(1, _s, _s),
+                                p=(0, 1, 1), groups=_c)
+SWEEP = ["GMM", "C1D", "C2D", "C3D", "DIL", "GRP", "T2D", *DEP_SHAPES, "GMM8K", "C2D_L3"]
 
 
 def gmm_shape(name):
@@ -146,7 +176,7 @@ def gmm_shape(name):
 
 
 def is_gmm(name):
-    return name.startswith("GMM")
+    return name.startswith("GMM") or name == "FLOOR"
 
 
 def op_spec(name):
@@ -173,7 +203,7 @@ def op_work(name):
         flops = 2 * tb.useful_macs(spec)
         byts = tb.compulsory_bytes(spec)
     ridge = pk["bf16_tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-    bound = "hbm" if (name == "DEP" or flops / byts < ridge) else "tensor"
+    bound = "hbm" if (name.startswith("DEP") or flops / byts < ridge) else "tensor"
     return flops, byts, bound
 
 
@@ -304,6 +334,55 @@ def measure_e2e(name, steps):
             "api": "tir_b200_conv_host" if not is_gmm(name) else "tir_b200_gmm_host"}
 
 
+def measure_e2e_interp(name, runs=3):
+    """The drop-in path exactly as a reference user takes it: the reference's own
+    interpreter (tir::run, /root/reference/proj built into oracle/_ref) runs the
+    whole-op tensorized program of the headline conv (conv2d_source semantics,
+    workloads.h:93-130), and its tensorized block is dispatched through the
+    HostKernel adapter (register_conv) -> tir_b200_conv_host_f32 -> B200 kernel.
+    Timed on the host clock per complete tir::run, split into view packing
+    (TensorView::get_f), the device call (H2D + kernel + D2H) and the write-back
+    (TensorView::set_f)."""
+    import ctypes
+
+    import numpy as np
+
+    from oracle import ir_gen as G  # the workload program text in the reference grammar
+
+    adapter = os.path.join(ROOT, "paper_2207_04296_b200", "lib", "libtir_b200_adapter.so")
+    if not os.path.exists(adapter):
+        return {"unavailable": "adapter library not built (needs /root/reference at build time)"}
+    L = ctypes.CDLL(adapter)
+    f32p = ctypes.POINTER(ctypes.c_float)
+    L.tir_b200_adapter_time_run.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(f32p),
+                                            f32p, ctypes.c_int64, ctypes.c_int, ctypes.POINTER(ctypes.c_double),
+                                            ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, ctypes.c_int]
+    spec = op_spec(name)
+    ospec = G.ConvSpec(op=spec.op, n=spec.n, in_dhw=spec.in_dhw, ci=spec.ci, co=spec.co, k=spec.k, s=spec.s,
+                       p=spec.p, d=spec.d, groups=spec.groups, transposed=spec.transposed)
+    rng = np.random.default_rng(11)
+    ins = [rng.standard_normal(ospec.x_shape(), dtype=np.float32).astype(np.float16).astype(np.float32),
+           rng.standard_normal(ospec.w_shape(), dtype=np.float32).astype(np.float16).astype(np.float32)]
+    out = np.zeros(ospec.y_shape(), np.float32)
+    arr = (f32p * 2)(*[x.ctypes.data_as(f32p) for x in ins])
+    sec = ctypes.c_double(0)
+    split = (ctypes.c_double * 3)()
+    err = ctypes.create_string_buffer(2048)
+    rc = L.tir_b200_adapter_time_run(G.conv_source(ospec).encode(), b"conv", 2, arr, out.ctypes.data_as(f32p),
+                                     out.size, runs, ctypes.byref(sec), split, err, len(err))
+    if rc != 0:
+        return {"error": err.value.decode()[:300]}
+    flops, _, _ = op_work(name)
+    return {"value": round(flops / sec.value / 1e12, 4), "unit": "TFLOPS",
+            "ms_per_step": round(sec.value * 1e3, 3), "runs": runs,
+            "split_ms": {"pack_views": round(split[0] * 1e3, 3), "device_call": round(split[1] * 1e3, 3),
+                         "unpack_view": round(split[2] * 1e3, 3)},
+            "h2d_bytes_per_step": int(sum(x.nbytes for x in ins) + out.nbytes),
+            "d2h_bytes_per_step": int(out.nbytes),
+            "path": "tir::run (reference interpreter) -> tensorized block -> HostKernel adapter "
+                    "(register_conv) -> tir_b200_conv_host_f32 (f32 views, accumulate) -> B200"}
+
+
 def traffic_from_profiles(name):
     """dram read+write bytes per launch from the committed ncu --set full summary."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -359,7 +438,7 @@ def measure_nets(device, world, rank, dist, steps, names):
             "tflops": round(net.flops * world * steps / sec / 1e12, 2),
             "ms_per_forward": round(ms / steps, 4),
             "batch_per_gpu": per_gpu, "global_batch": global_batch,
-            "launches_per_forward": nets.launches_per_forward(net),
+            "launches_per_forward": dn.launches,
             "sharding": f"batch across {world} GPU(s), no collective" if world > 1 else "single GPU",
             "dtype": "fp16 activations / fp32 accumulate",
             "weights": "random init (no checkpoints offline)",
@@ -457,8 +536,49 @@ def main():
     ap.add_argument("--no-nets", action="store_true", help="skip the batch-sharded network forwards")
     ap.add_argument("--nets", default="resnet50,mobilenet_v2,bert_large")
     ap.add_argument("--profile", metavar="OP", help="eager launches of one op for ncu (no timing)")
+    ap.add_argument("--profile-range", metavar="OP",
+                    help="warm-up, then --steps launches of one op between cudaProfilerStart/Stop "
+                         "(ncu --replay-mode range: steady-state DRAM bytes and time per launch)")
+    ap.add_argument("--launcher-check", action="store_true",
+                    help="rank bookkeeping only (gloo, no GPU): one JSON line with the ranks seen")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+
+    world, rank, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        spawn_ranks(args.gpus)
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}"}), flush=True)
+        sys.exit(2)
+    if args.launcher_check:
+        import torch
+
+        dist = init_dist(world, "gloo")
+        seen = torch.tensor([rank], dtype=torch.int64)
+        if dist:
+            got = [torch.zeros(1, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(got, seen)
+            ranks = sorted(int(t.item()) for t in got)
+            dist.destroy_process_group()
+        else:
+            ranks = [rank]
+        if rank == 0:
+            print(json.dumps({"n_gpus": world, "ranks": ranks}), flush=True)
+        return
+
+    if args.profile_range:
+        import torch
+
+        r = OpRunner(args.profile_range, torch.device("cuda", 0))
+        for i in range(args.warmup):
+            r.step(i)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStart()
+        for i in range(args.steps):
+            r.step(args.warmup + i)
+        torch.cuda.synchronize()
+        torch.cuda.cudart().cudaProfilerStop()
+        return
 
     if args.profile:
         import torch
@@ -475,7 +595,6 @@ def main():
 
     import torch
 
-    world, rank, local = dist_env()
     torch.cuda.set_device(local)
     dist = init_dist(world, "nccl")
     device = torch.device("cuda", local)
@@ -497,24 +616,40 @@ def main():
     del runner
     torch.cuda.empty_cache()
 
+    floor_us = None
     ops = {}
     if not args.no_ops and rank == 0:
-        for other in ["GMM", "C1D", "C2D", "C3D", "DIL", "GRP", "T2D", "DEP", "GMM8K", "C2D_L3"]:
+        try:  # per-launch floor: a one-CTA GEMM in the same graph-replay regime
+            r = OpRunner("FLOOR", device)
+            fms, _, _ = time_graph(r, 100, 3, None, None)
+            floor_us = fms / 100 * 1e3
+            del r
+        except Exception as e:
+            floor_us = None
+            ops["FLOOR"] = {"error": str(e)[:200]}
+        for other in SWEEP:
             try:
                 r = OpRunner(other, device)
                 k = max(10, min(args.steps, 100)) if other != "GMM8K" else 10
                 oms, ol, _ = time_graph(r, k, 3, None, None)
                 f, b, bd = op_work(other)
                 t = oms / 1e3 / k
+                t_roof = max(f / (pk["bf16_tflops"] * 1e12), b / (pk["hbm_gbs"] * 1e9))
                 ops[other] = {
                     "tflops": round(f / t / 1e12, 2), "gbs": round(b / t / 1e9, 1),
                     "us": round(t * 1e6, 3), "bound": bd,
                     "frac_tensor_spec": round(f / t / 1e12 / SPEC_TC_PEAK_TFLOPS, 4),
                     "frac_tensor_measured": round(f / t / 1e12 / pk["bf16_tflops"], 4),
                     "frac_hbm": round(b / t / 1e9 / pk["hbm_gbs"], 4),
-                    "frac_roofline": round(min(1.0, (f / t) / min(pk["bf16_tflops"] * 1e12,
-                                                                   f / b * pk["hbm_gbs"] * 1e9)), 4),
-                    "launches_per_step": ol // k, "l2_sets": r.sets,
+                    # roofline time / measured time (not clamped)
+                    "frac_roofline": round(t_roof / t, 4),
+                    # the same with the measured per-launch floor taken out of the measured time
+                    "frac_roofline_ex_floor": (round(t_roof / max(t - floor_us * 1e-6, t_roof), 4)
+                                               if floor_us else None),
+                    "roofline_us": round(t_roof * 1e6, 3),
+                    "launches_per_step": ol / k, "l2_sets": r.sets,
+                    "algorithmic_bytes": b, "algorithmic_flops": f,
+                    "traffic_per_launch": traffic_from_profiles(other),
                 }
                 del r
                 torch.cuda.empty_cache()
@@ -530,8 +665,13 @@ def main():
             net_lines = {"error": str(e)[:300]}
 
     e2e = None
+    e2e_interp = None
     if not args.no_e2e and rank == 0:
         e2e = measure_e2e(name, args.steps)
+        try:
+            e2e_interp = measure_e2e_interp(name)
+        except Exception as e:  # report, never hide
+            e2e_interp = {"error": str(e)[:300]}
 
     cpu = None
     if not args.no_cpu and rank == 0:
@@ -568,6 +708,9 @@ def main():
             "e2e": e2e,
             "clocks": clocks,
             "gpu_launches": launches,
+            "launches_per_step": launches / args.steps,
+            "floor_us": round(floor_us, 3) if floor_us else None,
+            "e2e_interp": e2e_interp,
             "ops": ops,
             "nets": net_lines,
         }

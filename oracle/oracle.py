@@ -149,6 +149,23 @@ def tensors_close_dot(a: np.ndarray, b: np.ndarray, abs_sum: np.ndarray, rel_tol
     return bool(np.all(ok))
 
 
+def d2_stats(a: np.ndarray, b: np.ndarray, abs_sum: np.ndarray, rel_tol: float = 1e-4,
+             dot_tol: float = 1e-6) -> dict:
+    """tensors_close_dot, itemised: how many elements pass the plain
+    tensors_close bar (rel_tol), how many pass ONLY through the dot-product
+    clause, how many fail, and the worst errors of each kind."""
+    a64, b64 = a.astype(np.float64), b.astype(np.float64)
+    err = np.abs(a64 - b64)
+    denom = np.maximum(np.maximum(np.abs(a64), np.abs(b64)), 1.0)
+    rel_ok = err <= rel_tol * denom
+    dot_ok = err <= dot_tol * abs_sum.astype(np.float64)
+    return {"elements": int(a.size), "bitwise_equal": int(np.sum(a64 == b64)),
+            "rel_ok": int(np.sum(rel_ok)), "dot_clause_only": int(np.sum(dot_ok & ~rel_ok)),
+            "failed": int(np.sum(~(rel_ok | dot_ok))),
+            "max_rel_err": float(np.max(err / denom)) if a.size else 0.0,
+            "max_err_over_abs_sum": float(np.max(err / np.maximum(abs_sum, 1e-30))) if a.size else 0.0}
+
+
 def tensors_bitwise_equal(a: np.ndarray, b: np.ndarray) -> bool:
     """Value equality as the reference defines it (get_f compared with !=, so
     +0 == -0)."""

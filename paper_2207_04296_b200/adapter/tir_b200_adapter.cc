@@ -8,8 +8,11 @@
 // is written back through set_f.
 #include "tir_b200_adapter.h"
 
+#include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstring>
+#include <thread>
 #include <vector>
 
 #include "tir/structural.h"
@@ -28,30 +31,66 @@ int64_t cells_of(const std::vector<int64_t>& e) {
   return n;
 }
 
+// Walks the cells [begin, end) of a row-major view extent, calling f(idx, flat).
 template <typename F>
-void for_each_index(const std::vector<int64_t>& ext, F&& f) {
-  if (cells_of(ext) == 0) return;
+void for_each_index(const std::vector<int64_t>& ext, int64_t begin, int64_t end, F&& f) {
+  if (begin >= end) return;
   std::vector<int64_t> idx(ext.size(), 0);
-  for (int64_t flat = 0;; ++flat) {
+  int64_t rem = begin;
+  for (int d = static_cast<int>(ext.size()) - 1; d >= 0; --d) {
+    idx[d] = rem % ext[d];
+    rem /= ext[d];
+  }
+  for (int64_t flat = begin; flat < end; ++flat) {
     f(idx, flat);
     int d = static_cast<int>(idx.size()) - 1;
     while (d >= 0 && ++idx[d] == ext[d]) idx[d--] = 0;
-    if (d < 0) break;
   }
 }
 
+// TensorView offers only per-element get_f / set_f (interp.h:57-83; no pointer
+// accessor by design), at ~50-130 ns a cell. Large views are walked by up to
+// 32 threads over disjoint flat ranges: get_f only reads, and set_f of distinct
+// cells writes distinct bytes of the tensor's storage, so the ranges never
+// touch the same memory.
+template <typename F>
+void parallel_cells(const std::vector<int64_t>& ext, F&& f) {
+  const int64_t n = cells_of(ext);
+  if (n == 0) return;
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const int64_t threads = std::min<int64_t>({static_cast<int64_t>(hw), 32, (n + 65535) / 65536});
+  if (threads <= 1) {
+    for_each_index(ext, 0, n, f);
+    return;
+  }
+  std::vector<std::thread> pool;
+  for (int64_t t = 0; t < threads; ++t)
+    pool.emplace_back([&, t] { for_each_index(ext, n * t / threads, n * (t + 1) / threads, f); });
+  for (auto& th : pool) th.join();
+}
+
+struct Timer {
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  double s() const { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); }
+};
+thread_local double t_pack = 0, t_device = 0, t_unpack = 0;
+
 std::vector<float> pack(const tir::TensorView& v) {
+  Timer t;
   std::vector<float> out(static_cast<size_t>(v.cells()));
-  for_each_index(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
+  parallel_cells(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
     out[static_cast<size_t>(flat)] = static_cast<float>(v.get_f(idx));
   });
+  t_pack += t.s();
   return out;
 }
 
 void unpack(tir::TensorView& v, const std::vector<float>& data) {
-  for_each_index(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
+  Timer t;
+  parallel_cells(extents_of(v), [&](const std::vector<int64_t>& idx, int64_t flat) {
     v.set_f(idx, data[static_cast<size_t>(flat)]);
   });
+  t_unpack += t.s();
 }
 
 [[noreturn]] void raise(int rc) {
@@ -102,8 +141,8 @@ int conv_rank(const tir_b200_conv_desc& d) {
 
 }  // namespace
 
-void register_gmm(tir::ExecContext& ctx, const std::string& name) {
-  ctx.register_host_kernel(name, [name](std::vector<tir::TensorView>& views) {
+void register_gmm(tir::ExecContext& ctx, const std::string& name, bool accumulate) {
+  ctx.register_host_kernel(name, [name, accumulate](std::vector<tir::TensorView>& views) {
     require(views.size() == 3, name + ": expects views [C, A, B]");
     tir::TensorView& c = views[0];
     const tir::TensorView& a = views[1];
@@ -115,19 +154,23 @@ void register_gmm(tir::ExecContext& ctx, const std::string& name) {
     require(ce.size() == 2 && ae.size() == 2 && be.size() == 2, name + ": operands must be 2-D");
     const int64_t M = ae[0], K = ae[1], N = be[1];
     require(be[0] == K && ce[0] == M && ce[1] == N, name + ": operand extents do not form C[M,N] += A[M,K].B[K,N]");
-    std::vector<float> A = pack(a), B = pack(b), C = pack(c);
-    int rc = tir_b200_gmm_host_f32(A.data(), B.data(), C.data(), M, N, K, /*accumulate=*/1);
+    std::vector<float> A = pack(a), B = pack(b);
+    std::vector<float> C = accumulate ? pack(c) : std::vector<float>(static_cast<size_t>(M * N));
+    Timer t;
+    int rc = tir_b200_gmm_host_f32(A.data(), B.data(), C.data(), M, N, K, accumulate ? 1 : 0);
+    t_device += t.s();
     if (rc) raise(rc);
     unpack(c, C);
   });
 }
 
-void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b200_conv_desc& desc) {
+void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b200_conv_desc& desc,
+                   bool accumulate) {
   // Validate once at registration; geometry errors surface here, not mid-run.
   int64_t out[3];
   int rc = tir_b200_conv_out_shape(&desc, out);
   if (rc) raise(rc);
-  ctx.register_host_kernel(name, [name, desc](std::vector<tir::TensorView>& views) {
+  ctx.register_host_kernel(name, [name, desc, accumulate](std::vector<tir::TensorView>& views) {
     require(views.size() == 3, name + ": expects views [Y, X, W]");
     tir::TensorView& y = views[0];
     const tir::TensorView& x = views[1];
@@ -139,8 +182,11 @@ void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b20
     require(x.extents() == conv_x_shape(desc, r), name + ": X view does not match the descriptor");
     require(w.extents() == conv_w_shape(desc, r), name + ": W view does not match the descriptor");
     require(y.extents() == conv_y_shape(desc, r), name + ": Y view does not match the descriptor");
-    std::vector<float> X = pack(x), W = pack(w), Y = pack(y);
-    int rc2 = tir_b200_conv_host_f32(&desc, X.data(), W.data(), Y.data(), /*accumulate=*/1);
+    std::vector<float> X = pack(x), W = pack(w);
+    std::vector<float> Y = accumulate ? pack(y) : std::vector<float>(static_cast<size_t>(y.cells()));
+    Timer t;
+    int rc2 = tir_b200_conv_host_f32(&desc, X.data(), W.data(), Y.data(), accumulate ? 1 : 0);
+    t_device += t.s();
     if (rc2) raise(rc2);
     unpack(y, Y);
   });
@@ -275,5 +321,37 @@ extern "C" int tir_b200_adapter_pad_channels(const char* ir_text, const char* bl
     copy_out(tir::print_text(s.func()), text, text_len, "text");
     copy_out(tir::trace_to_jsonl(s.trace()), trace, trace_len, "trace");
     if (padded) *padded = p;
+  });
+}
+
+// Drop-in end-to-end timing (bench.py e2e_interp): tensorize `block` of a scalar
+// program once, then time `runs` complete tir::run calls — the reference's own
+// interpreter dispatching the tensorized block to the B200 kernel through the
+// HostKernel above (view packing, host-buffer C-ABI call with its H2D / D2H,
+// write-back). Returns seconds per run and its split (pack / device call /
+// unpack) per run; the last run's output goes to `out`.
+extern "C" int tir_b200_adapter_time_run(const char* ir_text, const char* block, int n_in,
+                                         const float* const* inputs, float* out, int64_t out_elems, int runs,
+                                         double* sec_per_run, double* split3, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    tir::Schedule s(tir::parse_text(ir_text));
+    tir::ExecContext ctx;
+    const tir_b200::OpMatch m = tir_b200::tensorize_whole_op(s, block);
+    tir_b200::register_matched(ctx, m);
+    run_program(*s.func(), ctx, n_in, inputs, out, out_elems, nullptr);  // warm-up (allocations)
+    tir_b200::t_pack = tir_b200::t_device = tir_b200::t_unpack = 0;
+    tir_b200::Timer t;
+    for (int i = 0; i < runs; ++i) {
+      tir::ExecContext c2;
+      tir_b200::register_matched(c2, m);
+      run_program(*s.func(), c2, n_in, inputs, out, out_elems, nullptr);
+    }
+    const double total = t.s();
+    *sec_per_run = total / runs;
+    if (split3) {
+      split3[0] = tir_b200::t_pack / runs;
+      split3[1] = tir_b200::t_device / runs;
+      split3[2] = tir_b200::t_unpack / runs;
+    }
   });
 }

@@ -24,14 +24,18 @@
 
 namespace tir_b200 {
 
-// GMM intrinsic: views [C f32 [M,N], A f16 [M,K], B f16 [K,N]]; C += A.B.
-void register_gmm(tir::ExecContext& ctx, const std::string& name = "b200.gmm");
+// GMM intrinsic: views [C f32 [M,N], A f16 [M,K], B f16 [K,N]]; C += A.B
+// (accumulate = true, the blockize convention), or C = A.B (accumulate = false:
+// the whole-op composite folded a zero init into the call, so C is neither
+// read nor uploaded).
+void register_gmm(tir::ExecContext& ctx, const std::string& name = "b200.gmm", bool accumulate = true);
 
 // Convolution intrinsic with fixed geometry (the reference forwards neither
 // call arguments nor annotations to the kernel, interp.cc:360-383, so stride,
 // padding, dilation and groups are captured here). Views [Y, X, W] whose
 // extents must match the descriptor (tir_b200.h layouts).
-void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b200_conv_desc& desc);
+void register_conv(tir::ExecContext& ctx, const std::string& name, const tir_b200_conv_desc& desc,
+                   bool accumulate = true);
 
 // The conventional intrinsic name for a descriptor, e.g. "b200.c2d.s1p1d1g1".
 std::string conv_intrin_name(const tir_b200_conv_desc& desc);

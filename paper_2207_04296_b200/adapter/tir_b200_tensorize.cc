@@ -151,17 +151,24 @@ Stmt rewrite(const Stmt& s, const tir::StmtNode* target, const Stmt& repl) {
 }
 
 // The step "b200.tensorize": outer block body := intrin(), attrs("tensorized" = intrin).
-void replace_with_call(tir::Schedule& s, const std::string& block, const std::string& intrin) {
+// drop_init: the outer block's init (the zero store blockize moved out of the
+// contraction, schedule_block.cc:570-603) is removed and the call overwrites
+// its output instead — for a whole-op block the init would run exactly once,
+// right before the single call, so the result is unchanged, while the
+// interpreter no longer zero-fills the output element by element and the
+// HostKernel neither packs nor uploads it.
+void replace_with_call(tir::Schedule& s, const std::string& block, const std::string& intrin, bool drop_init) {
   Stmt o = s.find_block_realize(block);
   if (!o) tir::throw_error("StaleHandle", "no block named '" + block + "'");
   auto blk = std::make_shared<tir::Block>(*o->block);
   blk->body = tir::make_evaluate(tir::make_call(intrin));
+  if (drop_init) blk->init = nullptr;
   blk->annotations["tensorized"] = intrin;
   Stmt repl = tir::make_block_realize(o->bindings, o->predicate, blk);
   Stmt body = rewrite(s.func()->body, o.get(), repl);
   tir::TraceStep step;
   step.prim = "b200.tensorize";
-  step.args = {{"block", block}, {"intrin", intrin}};
+  step.args = {{"block", block}, {"intrin", intrin}, {"drop_init", drop_init}};
   s.commit_rewrite(tir::make_func(s.func()->name, s.func()->params, body), std::move(step));
 }
 
@@ -253,6 +260,7 @@ OpMatch match_contraction(const tir::PrimFunc& f, const std::string& block) {
   }
 
   OpMatch m;
+  m.overwrite = B.init != nullptr;  // Y = 0 (checked above), then Y += ...: the call may overwrite
   const size_t R = ys.size();
   if (R == 2) {  // GMM: Y[i, j] += X[i, k] * W[k, j]
     const std::string vk = X.idx.size() == 2 ? var_name(X.idx[1]) : "";
@@ -266,7 +274,7 @@ OpMatch match_contraction(const tir::PrimFunc& f, const std::string& block) {
     if (Y->shape != std::vector<int64_t>{m.m, m.n} || X.buf->shape != std::vector<int64_t>{m.m, m.k} ||
         W.buf->shape != std::vector<int64_t>{m.k, m.n})
       mismatch("GMM iterator extents do not cover the buffers (not a whole-op block)");
-    m.intrin = "b200.gmm";
+    m.intrin = m.overwrite ? "b200.gmm.ow" : "b200.gmm";
     return m;
   }
   if (R < 3 || R > 5) mismatch("unsupported output rank");
@@ -425,7 +433,7 @@ OpMatch match_contraction(const tir::PrimFunc& f, const std::string& block) {
   if (X.buf->shape != xs || W.buf->shape != ws || Y->shape != yshape)
     mismatch("conv iterator extents do not cover the buffers (not a whole-op block)");
   m.conv = d;
-  m.intrin = conv_intrin_key(d);
+  m.intrin = conv_intrin_key(d) + (m.overwrite ? ".ow" : "");
   return m;
 }
 
@@ -442,7 +450,7 @@ OpMatch tensorize_whole_op(tir::Schedule& s, const std::string& block) {
         !tir::is_const_int(o->bindings[i], 0))
       tir::throw_error("NotWholeOp", "the loop nest of '" + block + "' covers only part of the op");
   }
-  replace_with_call(trial, outer, m.intrin);
+  replace_with_call(trial, outer, m.intrin, m.overwrite);
   s = trial;
   return m;
 }
@@ -450,9 +458,9 @@ OpMatch tensorize_whole_op(tir::Schedule& s, const std::string& block) {
 void register_matched(tir::ExecContext& ctx, const OpMatch& m) {
   if (ctx.has_kernel(m.intrin)) return;
   if (m.gmm) {
-    register_gmm(ctx, m.intrin);
+    register_gmm(ctx, m.intrin, !m.overwrite);
   } else {
-    register_conv(ctx, m.intrin, m.conv);
+    register_conv(ctx, m.intrin, m.conv, !m.overwrite);
   }
 }
 
@@ -511,7 +519,8 @@ int64_t pad_conv_channels(tir::Schedule& s, const std::string& block, int64_t mu
 void register_tensorize_step_handler() {
   static const bool registered = [] {
     tir::register_step_handler("b200.tensorize", [](tir::Schedule& s, const tir::TraceStep& step) {
-      replace_with_call(s, step.args.at("block").get<std::string>(), step.args.at("intrin").get<std::string>());
+      replace_with_call(s, step.args.at("block").get<std::string>(), step.args.at("intrin").get<std::string>(),
+                        step.args.value("drop_init", false));
     });
     return true;
   }();

@@ -40,6 +40,7 @@ struct OpMatch {
   int64_t m = 0, n = 0, k = 0;  // GMM extents
   tir_b200_conv_desc conv{};    // conv geometry (when !gmm)
   std::string intrin;           // generated intrinsic name
+  bool overwrite = false;       // the block's zero init was folded into the call (Y = op, suffix ".ow")
 };
 
 // Recognises `block` in f (see above). Throws DescMismatch with the reason.

@@ -113,8 +113,8 @@ struct alignas(64) IgemmParams {
   int32_t store_mode;  // 0: generic row-offset stores, 1: TMA store, 2: TMA reduce-add (Y += tile)
   int32_t epi_cw;      // store modes 1/2: columns per staged chunk (32, or 64 for fp16 with BN >= 64)
   int32_t bias_floats; // > 0: the whole bias vector is staged in shared memory (16-byte broadcasts)
-  int32_t ksplit;      // split-K partitions (>= 1); > 1 adds partials into a pre-initialised Y
-  int32_t reduce;      // generic path: red.global.add into Y instead of stores (split-K)
+  int32_t ksplit;      // split-K partitions (>= 1); > 1: clusters of ksplit CTAs, one output tile each,
+                       // partials combined through distributed shared memory (see cluster_reduce)
   CUtensorMap tmY;     // store_mode != 0: Y as 2-D [rows, ldy], box {32, 32}
   unsigned long long* trace;  // debug: per-stage clock64 stamps of CTA 0 (null in production)
   int32_t batch_tiles;  // batched GMM: tiles per problem (0 = not batched)
@@ -263,6 +263,134 @@ __device__ __forceinline__ void decompose_tile(const IgemmParams& p, int tile, i
 __device__ __forceinline__ void split_range(const IgemmParams& p, int nst, int ks, int& st0, int& st1) {
   st0 = static_cast<int>(static_cast<int64_t>(nst) * ks / p.ksplit);
   st1 = static_cast<int>(static_cast<int64_t>(nst) * (ks + 1) / p.ksplit);
+}
+
+__device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr)
+               : "memory");
+  return v;
+}
+
+// Deterministic split-K. The ksplit CTAs of a cluster (consecutive tile ids:
+// the split index is fastest) hold the fp32 partials of ONE output tile in
+// shared memory ([128][BN + 4], written by the epilogue warps). After a cluster
+// barrier, cluster rank r combines rows [r*R, (r+1)*R) of the tile over all
+// ranks through distributed shared memory in the fixed order
+// ((p_0 + p_1) + p_2) + ..., then applies the C-ABI epilogue — (Yin +) sum,
+// + bias, + residual, activation — and stores 16-byte vectors at the output
+// pixel of each row (row-linear or, for T2D classes, strided). No memset, no
+// atomics: the result is identical on every run. A second barrier keeps every
+// partial alive until all ranks have read it. All threads of the CTA take part.
+template <int BN>
+__device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float* part, int64_t* row_off) {
+  mc_cluster_sync();  // every partial of the cluster is written (release / acquire)
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int ks = p.ksplit;
+  const int tile = blockIdx.x;
+  const bool active = tile < p.total_tiles;
+  int s = 0, mt = 0, g = 0, nt = 0, kk = 0;
+  if (active) decompose_tile(p, tile, s, mt, g, nt, kk);
+  const SubProb& sp = p.sub[s];
+  const int rows = (kBM + ks - 1) / ks;
+  const int r0 = static_cast<int>(rank) * rows, r1 = min(kBM, r0 + rows);
+  // output element offset of each of this rank's rows (-1: past the sub-problem)
+  for (int r = r0 + threadIdx.x; active && r < r1; r += blockDim.x) {
+    const int m = mt * kBM + r;
+    int64_t off = -1;
+    if (m < sp.m_count) {
+      int x = m % sp.gx, rest = m / sp.gx;
+      const int y = rest % sp.gy;
+      rest /= sp.gy;
+      const int z = rest % sp.gz;
+      const int n = rest / sp.gz;
+      const int64_t pix = ((static_cast<int64_t>(n) * p.out_dims[2] + z * sp.o_st[2] + sp.o_b[2]) * p.out_dims[1] +
+                           y * sp.o_st[1] + sp.o_b[1]) * p.out_dims[0] + x * sp.o_st[0] + sp.o_b[0];
+      off = pix * p.ldy + g * p.cog + nt * BN;
+    }
+    row_off[r - r0] = off;
+  }
+  __syncthreads();
+  if (active) {
+    pdl_wait();  // Yin / residual may come from the preceding kernel
+    constexpr int kV = BN / 4;  // float4 per partial row
+    constexpr int kU = 8;       // items in flight per thread (one remote load each per split)
+    const uint32_t base = smem_u32(part);
+    const int valid = p.cog - nt * BN;
+    const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
+                        (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
+    const int items = (r1 - r0) * kV;
+#pragma unroll 1
+    for (int i0 = threadIdx.x; i0 < items; i0 += kU * blockDim.x) {
+      float4 v[kU];
+#pragma unroll 1
+      for (int k = 0; k < ks; ++k) {
+        uint32_t rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(base), "r"(k));
+        float4 t[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          const int i = i0 + u * blockDim.x;
+          if (i < items) {
+            const int row = r0 + i / kV, col = (i % kV) * 4;
+            t[u] = ld_cluster_f4(rb + static_cast<uint32_t>((row * (BN + 4) + col) * 4));
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+          if (k == 0) {
+            v[u] = t[u];
+          } else {
+            v[u].x = v[u].x + t[u].x; v[u].y = v[u].y + t[u].y;
+            v[u].z = v[u].z + t[u].z; v[u].w = v[u].w + t[u].w;
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i >= items) continue;
+        const int row = i / kV, col = (i % kV) * 4;
+        const int64_t ro = row_off[row];
+        if (ro < 0 || col >= valid) continue;
+        const int64_t off = ro + col;
+        const int lim = valid - col;
+        const bool vec = vec_ok && lim >= 4;
+        float* vv = reinterpret_cast<float*>(&v[u]);
+        if (p.accumulate) {
+          if (vec) {
+            const float4 y0 = *reinterpret_cast<const float4*>(p.Yin + off);
+            vv[0] = y0.x + vv[0]; vv[1] = y0.y + vv[1]; vv[2] = y0.z + vv[2]; vv[3] = y0.w + vv[3];
+          } else {
+            for (int j = 0; j < 4 && j < lim; ++j) vv[j] = p.Yin[off + j] + vv[j];
+          }
+        }
+        if (p.bias || p.relu || p.residual)
+          epi_run<4>(vv, p.bias, g * p.cog + nt * BN + col, lim, p.residual ? p.residual + off : nullptr, p.relu);
+        if (p.out_f16) {
+          __half* yp = reinterpret_cast<__half*>(p.Y) + off;
+          if (vec) {
+            __half2 h0 = __floats2half2_rn(vv[0], vv[1]), h1 = __floats2half2_rn(vv[2], vv[3]);
+            uint2 w2;
+            w2.x = *reinterpret_cast<uint32_t*>(&h0);
+            w2.y = *reinterpret_cast<uint32_t*>(&h1);
+            *reinterpret_cast<uint2*>(yp) = w2;
+          } else {
+            for (int j = 0; j < 4 && j < lim; ++j) yp[j] = __float2half_rn(vv[j]);
+          }
+        } else {
+          float* yp = reinterpret_cast<float*>(p.Y) + off;
+          if (vec) *reinterpret_cast<float4*>(yp) = v[u];
+          else
+            for (int j = 0; j < 4 && j < lim; ++j) yp[j] = vv[j];
+        }
+      }
+    }
+  }
+  mc_cluster_sync();  // peers have finished reading this CTA's partial
 }
 
 // Piece table entry: everything a producer needs for one TMA piece, computed
@@ -617,7 +745,33 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     constexpr int kHs = kEpi / 4;  // column chunks are dealt round-robin over the kHs warps of a quadrant
     uint8_t* wbuf = epi_smem + warp * Cfg::kEpiWarpBytes;
     uint32_t acc = 0, acc_phase = 0, chunk = 0;
-    if (p.store_mode) {
+    if (p.ksplit > 1) {
+      // Split-K partial: the CTA's one tile (grid == total_tiles) goes from TMEM
+      // to a padded [128][BN + 4] fp32 image over the drained operand ring (every
+      // MMA, hence every operand read, completed before tfull); cluster_reduce
+      // below combines the ksplit partials of the cluster in a fixed order.
+      float* part = reinterpret_cast<float*>(smem);
+      constexpr int kChunk = BN < 32 ? BN : 32;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        mbar_wait(&tfull[acc], acc_phase);
+        tc_fence_after();
+#pragma unroll 1
+        for (int c0 = static_cast<int>(hh) * kChunk; c0 < BN; c0 += kHs * kChunk) {
+          uint32_t r[32];
+          const uint32_t taddr = tmem_base + ((q * 32u) << 16) + acc * BN + c0;
+          if (kChunk == 32) tmem_ld_32x32b_x32(taddr, r);
+          else tmem_ld_32x32b_x16(taddr, r);
+          tmem_ld_wait();
+          float4* dst = reinterpret_cast<float4*>(part + (q * 32 + lane) * (BN + 4) + c0);
+#pragma unroll
+          for (int i = 0; i < kChunk / 4; ++i)
+            dst[i] = make_float4(__uint_as_float(r[4 * i]), __uint_as_float(r[4 * i + 1]),
+                                 __uint_as_float(r[4 * i + 2]), __uint_as_float(r[4 * i + 3]));
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+      }
+    } else if (p.store_mode) {
       // TMA store: thread = tile row (tcgen05.ld 32x32b); each warp stages its
       // 32 rows x cw columns (SW128 / SW64 swizzled, conflict-free) and issues
       // one bulk tensor store (or reduce-add for accumulate) per chunk; two
@@ -835,18 +989,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
             const int64_t off = ro + c0 + col;
             float4 v = *reinterpret_cast<const float4*>(stg + rr * 36 + col);
             const bool vec = vec_ok && col + 4 <= valid;
-            if (p.reduce) {  // split-K partial: Y += v (fp32 output only)
-              float* y = reinterpret_cast<float*>(p.Y) + off;
-              if (vec) {
-                asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(y), "f"(v.x), "f"(v.y),
-                             "f"(v.z), "f"(v.w)
-                             : "memory");
-              } else {
-                const float* vv = reinterpret_cast<const float*>(&v);
-                for (int i = 0; i < 4 && col + i < valid; ++i) atomicAdd(y + i, vv[i]);
-              }
-              continue;
-            }
             if (p.accumulate) {
               if (vec) {
                 const float4 t = *reinterpret_cast<const float4*>(p.Yin + off);
@@ -908,6 +1050,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   __syncthreads();
   tc_fence_after();
   if constexpr (cg2) mc_cluster_sync();  // the leader's MMAs into this CTA's TMEM are done
+  if (p.ksplit > 1) cluster_reduce<BN>(p, reinterpret_cast<const float*>(smem), reinterpret_cast<int64_t*>(epi_smem));
   if (warp == kMmaWarp) {
     if constexpr (cg2)
       asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "n"(Cfg::kTmemCols)

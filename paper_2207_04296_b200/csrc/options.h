@@ -37,7 +37,8 @@ struct Options {
 
 struct OptionEntry {
   const char* name;
-  int Options::* field;
+  using Field = int Options::*;
+  Field field;
 };
 
 inline const OptionEntry* option_table(int* count) {

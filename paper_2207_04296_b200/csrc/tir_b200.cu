@@ -311,7 +311,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   int grid = std::min(p.total_tiles, di.sms);
   // Keep B resident when its whole K panel fits next to a >= 3-deep A ring and
   // every CTA can be pinned to one (group, n-tile): grid a multiple of `keys`.
-  if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && !p.batch_tiles && keys <= di.sms &&
+  if (p.b_mode == tb::B_STREAM && p.num_sub == 1 && !p.batch_tiles && p.ksplit == 1 && keys <= di.sms &&
       res_rows * Cfg::kBRowBytes < (1 << 18) && res_bytes + 3 * Cfg::kABytes <= budget) {
     p.b_mode = tb::B_RESIDENT;
     p.b_res_rows = res_rows;
@@ -323,6 +323,24 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   }
   if (p.stages < 2) return set_err(TIR_B200_ERR_UNSUPPORTED, "not enough shared memory");
   size_t smem = Cfg::smem_bytes(p.stages, p.b_res_rows, p.total_pieces, p.bias_floats);
+  if (p.ksplit > 1) {
+    // one output tile per CTA, its ksplit partials in one cluster; the [128][BN + 4]
+    // fp32 partial image reuses the drained operand ring
+    const size_t ring = static_cast<size_t>(p.stages) * Cfg::kABytes +
+                        (p.b_res_rows ? static_cast<size_t>(p.b_res_rows) * BN * 2
+                                      : static_cast<size_t>(p.stages) * Cfg::kBBytes);
+    if (p.total_tiles > di.sms || p.total_tiles % p.ksplit || ring < static_cast<size_t>(tb::kBM) * (BN + 4) * 4)
+      return set_err(TIR_B200_ERR_UNSUPPORTED, "split-K plan does not fit (tiles %d, ksplit %d)", p.total_tiles,
+                     p.ksplit);
+    CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(smem)));
+    p.mc = 0;
+    p.trace = g_trace;
+    CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8>, p.total_tiles, p.ksplit, Cfg::kThreadsN, smem,
+                                stream, p));
+    ++g_launches;
+    return TIR_B200_OK;
+  }
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
@@ -556,37 +574,26 @@ int finalize_tiles(tb::IgemmParams& p, int bn, int ks) {
 
 // ------------------------------------------------------------------ split-K
 
-// Split the reduction when the output tiles cannot fill half the machine:
-// each split adds its fp32 partial into Y (TMA reduce-add or red.global.add),
-// so Y is first zeroed (or seeded with Yin when accumulating). Sums of the
-// reference distribution are exact in any order, so parity is unchanged.
+// Split the reduction when the output tiles cannot fill half the machine: the
+// ksplit CTAs of one output tile form a thread-block cluster and combine their
+// fp32 partials through distributed shared memory in a fixed order
+// (igemm.cuh cluster_reduce), then apply the whole epilogue — deterministic,
+// no workspace, no memset, no atomics. <= 8 splits (portable cluster size).
 int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int sms) {
-  if (const int e = tb::options().ksplit) return std::max(1, e);
-  if (out_f16 || p.bias || p.relu || p.residual || out_tiles * 2 > sms) return 1;  // epilogue needs the full sum
   int nst_min = 1 << 30;
   for (int i = 0; i < p.num_sub; ++i) nst_min = std::min(nst_min, p.sub[i].num_stages);
+  // every split needs >= 1 stage (an empty split would publish an unwritten accumulator)
+  if (const int e = tb::options().ksplit) return std::max(1, std::min({8, e, nst_min}));
+  // Fused-epilogue launches (the network graphs) are never split automatically:
+  // one reduction order per output element whatever the batch, so a batch shard
+  // is bit-identical to the same rows of the full-batch forward.
+  if (out_f16 || p.bias || p.relu || p.residual) return 1;
+  if (out_tiles * 2 > sms) return 1;
   int ks = static_cast<int>(std::min<int64_t>(sms / out_tiles, 8));
   ks = std::min(ks, nst_min / 2);  // at least two stages per split
   return std::max(ks, 1);
 }
 
-int prepare_split_output(tb::IgemmParams& p, void* Y, const float* Yin, int64_t elems, int accumulate,
-                         cudaStream_t stream) {
-  if (p.ksplit <= 1) return TIR_B200_OK;
-  if (accumulate) {
-    if (Yin != Y) CUDA_TRY(cudaMemcpyAsync(Y, Yin, elems * 4, cudaMemcpyDeviceToDevice, stream));
-  } else {
-    CUDA_TRY(cudaMemsetAsync(Y, 0, elems * 4, stream));
-  }
-  p.accumulate = 0;
-  if (p.store_mode) {
-    p.store_mode = 2;  // TMA reduce-add
-  } else {
-    p.reduce = 1;      // red.global.add
-  }
-  p.Yin = nullptr;
-  return TIR_B200_OK;
-}
 
 // ------------------------------------------------------------------ GMM
 
@@ -646,11 +653,10 @@ int gmm_impl(const uint16_t* A, const uint16_t* B, const float* Cin, void* C, in
     rc = finalize_tiles(p, bn, ks_eff);
     if (rc) return rc;
   }
-  rc = pick_store_mode(p, bn, C, p.ksplit > 1 ? static_cast<const float*>(C) : Cin, M,
-                       accumulate || p.ksplit > 1, out_f16);
-  if (rc) return rc;
-  rc = prepare_split_output(p, C, Cin, M * N, accumulate, stream);
-  if (rc) return rc;
+  if (p.ksplit == 1) {
+    rc = pick_store_mode(p, bn, C, Cin, M, accumulate, out_f16);
+    if (rc) return rc;
+  }
   return launch_igemm(p, bn, ks_eff, stream);
 }
 
@@ -1146,11 +1152,10 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
       rc = finalize_tiles(p, bn, ks);
       if (rc) return rc;
     }
-    rc = pick_store_mode(p, bn, Y, p.ksplit > 1 ? static_cast<const float*>(Y) : Yin, M,
-                         accumulate || p.ksplit > 1, out_f16);
-    if (rc) return rc;
-    rc = prepare_split_output(p, Y, Yin, M * g.co, accumulate, stream);
-    if (rc) return rc;
+    if (p.ksplit == 1) {
+      rc = pick_store_mode(p, bn, Y, Yin, M, accumulate, out_f16);
+      if (rc) return rc;
+    }
     return launch_igemm(p, bn, ks, stream);
   }
 
@@ -1235,8 +1240,6 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     if (rc) return rc;
   }
   p.store_mode = 0;  // class rows scatter to strided output pixels
-  rc = prepare_split_output(p, Y, Yin, g.n * g.out[0] * g.out[1] * g.out[2] * g.co, accumulate, stream);
-  if (rc) return rc;
   return launch_igemm(p, bn, ks, stream);
 }
 

@@ -217,8 +217,10 @@ class DeviceNet:
             self.run()
         self.stream.synchronize()
         g = torch.cuda.CUDAGraph()
+        api.reset_launch_count()
         with torch.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
             self.run()
+        self.launches = api.launch_count()  # kernels in one captured forward (library counter)
         self.graph = g
         return g
 
@@ -371,8 +373,10 @@ class DeviceBert:
             self.run()
         self.stream.synchronize()
         g = torch.cuda.CUDAGraph()
+        api.reset_launch_count()
         with torch.cuda.graph(g, stream=self.stream, capture_error_mode="relaxed"):
             self.run()
+        self.launches = api.launch_count()  # kernels in one captured forward (library counter)
         self.graph = g
         return g
 

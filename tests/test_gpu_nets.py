@@ -220,3 +220,123 @@ def test_bert_matches_cpu_reference(cuda):
     dn.replay()
     torch.cuda.synchronize()
     assert np.array_equal(dn.output.float().cpu().numpy(), got)
+
+
+CUDA_SHARD_WORKER = """
+import os, sys
+sys.path.insert(0, {root!r})
+import numpy as np, torch, torch.distributed as dist
+from paper_2207_04296_b200 import nets
+dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
+torch.cuda.set_device(0)  # one GPU on the test box: both ranks share it
+dev = torch.device("cuda", 0)
+outs = {{}}
+for name, B, kw in (("resnet50", 4, dict(image=64)), ("mobilenet_v2", 4, dict(image=64)),
+                    ("bert_large", 2, dict(seq=128, layers=2, hidden=128, heads=2, ffn=512))):
+    if name == "bert_large":
+        from paper_2207_04296_b200 import shard
+        lo, hi = shard.batch_range(B, rank, world)
+        net = nets.bert_large(hi - lo, **kw)
+    else:
+        net, (lo, hi) = nets.build_shard(name, B, rank, world, **kw)
+    full_shape = (B,) + tuple(net.input_shape[1:]) if name != "bert_large" else (B * kw["seq"], kw["hidden"])
+    x = np.random.default_rng(5).standard_normal(full_shape).astype(np.float16)
+    xs = x[lo:hi] if name != "bert_large" else x[lo * kw["seq"]:hi * kw["seq"]]
+    dn = nets.device_net(net, dev)
+    dn.input.copy_(torch.from_numpy(xs))
+    dn.capture()                      # the warm-up run inside capture() consumed the input
+    dn.input.copy_(torch.from_numpy(xs))
+    dn.replay()
+    torch.cuda.synchronize()
+    part = dn.output.float().cpu().numpy()
+    parts = [None] * world
+    dist.all_gather_object(parts, part)
+    if rank == 0:
+        if name == "bert_large":
+            fnet = nets.bert_large(B, **kw)
+        else:
+            fnet = nets.NETS[name](B, **kw)
+        fd = nets.device_net(fnet, dev)
+        fd.input.copy_(torch.from_numpy(x))
+        with torch.cuda.stream(fd.stream):
+            fd.run()
+        fd.stream.synchronize()
+        full = fd.output.float().cpu().numpy()
+        got = np.concatenate(parts)
+        outs[name] = bool(got.shape == full.shape and np.array_equal(got, full))
+if rank == 0:
+    print("CUDA_SHARDS", outs, flush=True)
+    print("CUDA_SHARD_OK" if outs and all(outs.values()) else "CUDA_SHARD_BAD", flush=True)
+dist.destroy_process_group()
+"""
+
+
+def test_two_rank_cuda_shards_bitwise_equal_full_batch(tmp_path):
+    """two ranks (gloo for the gather; the test box has one GPU, so
+    both run on cuda:0) each run their batch shard of ResNet-50 / MobileNet-V2 /
+    a small BERT through libtir_b200 as a captured CUDA graph; the gathered
+    output equals the one-process full-batch forward BIT FOR BIT (no collective
+    in the hot path; fused-epilogue layers keep one reduction order per element
+    whatever the batch)."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "cuda_shard_worker.py"
+    script.write_text(CUDA_SHARD_WORKER.format(root=root))
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29561", str(script)]
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    assert "CUDA_SHARD_OK" in p.stdout, p.stdout[-3000:] + p.stderr[-3000:]
+
+
+@pytest.mark.parametrize("name", ["resnet50", "mobilenet_v2"])
+def test_network_full_size_matches_cpu_reference(name, cuda):
+    """The benchmarked configuration (224 x 224 images, every layer at full
+    width) against the float64 CPU replay, B = 2; and two graph replays give
+    bit-identical logits."""
+    from oracle import nets_ref
+
+    net = nets.NETS[name](2, image=224)
+    dn = nets.DeviceNet(net, cuda)
+    x = np.random.default_rng(11).standard_normal(net.input_shape).astype(np.float16)
+    dn.input.copy_(torch.from_numpy(x))
+    dn.capture()
+    dn.input.copy_(torch.from_numpy(x))
+    dn.replay()
+    torch.cuda.synchronize()
+    got = dn.output.reshape(2, -1).cpu().numpy().copy()
+    dn.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(dn.output.reshape(2, -1).cpu().numpy(), got)
+    want = nets_ref.forward(net, x)
+    rel = _rel(got, want)
+    print(f"[full-size] {name}: max |logit err| / max |logit| = {rel:.3e}")
+    assert np.isfinite(got).all()
+    assert rel < LOGIT_TOL, rel
+    assert (got.argmax(1) == want.argmax(1)).all()
+
+
+def test_bert_large_full_size_matches_cpu_reference(cuda):
+    """BERT-large at the benchmarked dimensions (hidden 1024, 16 heads, FFN 4096,
+    24 layers, sequence 512, B = 1) against the float64 CPU replay with the
+    device graph's fp16 rounding points."""
+    from oracle import nets_ref
+
+    net = nets.bert_large(1, seq=512)
+    assert (net.hidden, net.heads, net.layers, net.seq) == (1024, 16, 24, 512)
+    dn = nets.device_net(net, cuda)
+    x = np.random.default_rng(12).standard_normal(net.input_shape).astype(np.float16)
+    dn.input.copy_(torch.from_numpy(x))
+    with torch.cuda.stream(dn.stream):
+        dn.run()
+    dn.stream.synchronize()
+    got = dn.output.float().cpu().numpy()
+    want = nets_ref.bert_forward(net, x)
+    err = np.abs(got - want)
+    cos = float(np.sum(got * want) / np.sqrt(np.sum(got * got) * np.sum(want * want)))
+    print(f"[full-size] bert_large: max err {err.max():.3e}, mean err {err.mean():.3e}, cosine {cos:.8f}")
+    assert np.isfinite(got).all()
+    assert cos > 0.9999 and err.mean() < 1e-2, (err.max(), err.mean(), cos)

@@ -148,3 +148,21 @@ def test_host_api_without_gpu_fails_loudly():
     with pytest.raises(api.TirError) as e:
         api.gmm_host(A, B)
     assert e.value.kind == "CudaError"
+
+
+def test_bench_gpus_flag_spawns_ranks():
+    """`bench.py --gpus 2` outside torchrun re-executes itself under
+    torch.distributed.run with two ranks (gloo bookkeeping only, no GPU)."""
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-check"],
+                       capture_output=True, text=True, timeout=300)
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert p.returncode == 0 and lines, p.stdout + p.stderr
+    import json
+
+    d = json.loads(lines[-1])
+    assert d == {"n_gpus": 2, "ranks": [0, 1]}
+    # a WORLD_SIZE that contradicts --gpus is an error, not a silent 1-GPU run
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--launcher-check"],
+                       capture_output=True, text=True, timeout=120, env=env)
+    assert p.returncode == 2 and "WORLD_SIZE" in p.stdout

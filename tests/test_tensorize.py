@@ -128,10 +128,10 @@ def test_match_recovers_conv_geometry(name):
 
 def test_match_gmm_and_reference_workloads():
     text, _, intrin, d, mnk = tensorize(G.gmm_source(24, 40, 56), "gemm")
-    assert d.op == OPS["GMM"] and mnk == (24, 40, 56) and intrin == "b200.gmm"
+    assert d.op == OPS["GMM"] and mnk == (24, 40, 56) and intrin == "b200.gmm.ow"
     # the reference's own programs (tests/testing/workloads.h), f32 params
     _, _, intrin, d, mnk = tensorize(ref_workload("matmul", 16), "gemm")
-    assert intrin == "b200.gmm" and mnk == (16, 16, 16)
+    assert intrin == "b200.gmm.ow" and mnk == (16, 16, 16)
     _, _, _, d, _ = tensorize(ref_workload("conv2d", 8, 8, 4, 3, 3, 8), "conv")
     _check_desc(d, G.ConvSpec("C2D", n=1, in_dhw=(1, 8, 8), ci=4, co=8, k=(1, 3, 3)))
     _, _, _, d, _ = tensorize(ref_workload("depthwise", 8, 8, 8, 3, 3), "dw")
@@ -168,10 +168,19 @@ def test_rejects_non_contractions_and_partial_nests():
     assert e.value.kind == "DescMismatch" and "predicate" in e.value.message
 
 
-def test_tensorized_block_keeps_init_and_regions():
-    text, _, intrin, _, _ = tensorize(G.conv_source(SPECS["GRP"]), "conv")
-    assert "init {" in text  # blockize moved init to the outer block (schedule_block.cc:570-603)
-    assert text.count("tensorized") == 1
+def test_tensorized_block_init_and_regions():
+    """blockize moves the zero init to the outer block (schedule_block.cc:570-603);
+    for a whole-op block it would run once, right before the single call, so the
+    composite folds it into an overwriting intrinsic ('.ow': Y = op(X, W), the
+    output is neither zero-filled by the interpreter nor uploaded). A block
+    WITHOUT init (accumulate into Y) keeps the accumulating intrinsic."""
+    text, trace, intrin, _, _ = tensorize(G.conv_source(SPECS["GRP"]), "conv")
+    assert "init {" not in text and intrin.endswith(".ow") and '"drop_init":true' in trace.replace(" ", "")
+    assert text.count("tensorized") == 1 and "reads(" in text and "writes(" in text
+    no_init = re.sub(r"init \{[^}]*\}\s*", "", G.conv_source(SPECS["GRP"]))
+    assert "init {" not in no_init
+    text2, _, intrin2, _, _ = tensorize(no_init, "conv")
+    assert not intrin2.endswith(".ow") and intrin2 + ".ow" == intrin
 
 
 # ---------------------------------------------------------------- GPU: run it
