@@ -377,10 +377,13 @@ def measure_e2e_interp(name, runs=3):
             "ms_per_step": round(sec.value * 1e3, 3), "runs": runs,
             "split_ms": {"pack_views": round(split[0] * 1e3, 3), "device_call": round(split[1] * 1e3, 3),
                          "unpack_view": round(split[2] * 1e3, 3)},
-            "h2d_bytes_per_step": int(sum(x.nbytes for x in ins) + out.nbytes),
+            "h2d_bytes_per_step": int(sum(x.nbytes for x in ins)),
             "d2h_bytes_per_step": int(out.nbytes),
-            "path": "tir::run (reference interpreter) -> tensorized block -> HostKernel adapter "
-                    "(register_conv) -> tir_b200_conv_host_f32 (f32 views, accumulate) -> B200"}
+            "path": "tir::run (reference interpreter) -> whole-op tensorized block (zero init folded: "
+                    "overwriting intrinsic) -> HostKernel adapter (register_conv) -> tir_b200_conv_host_f32 "
+                    "(f32 views converted to fp16 on the device) -> B200",
+            "rest_ms": "tir::run itself: TensorValue allocation / zero-fill and copies of the "
+                       "interpreter's input and output tensors"}
 
 
 def traffic_from_profiles(name):

@@ -57,6 +57,7 @@ struct alignas(64) HaloParams {
   void* Y;
   const float* Yin;
   unsigned long long* trace;
+  int32_t l2_prefetch;  // first tile -> L2 before griddepcontrol.wait (ptx.cuh tma_prefetch_*)
 };
 
 template <int BN>
@@ -142,6 +143,16 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   if (warp == 8) {
     // ------------------------------------------------------------ producer
     if (elect_one()) {
+      if (p.l2_prefetch && static_cast<int>(blockIdx.x) < p.total_tiles) {
+        // first tile's slabs and the weight panel -> L2 before the wait (ptx.cuh tma_prefetch_*)
+        int n, th, tw, g, nt;
+        decompose(blockIdx.x, n, th, tw, g, nt);
+        for (int cb = 0; cb < p.cblocks && cb < S; ++cb)
+          tma_prefetch_4d(&p.tmX, g * p.cig + cb * 64, tw * p.Wt - p.pad_w, th * p.R - p.pad_h, n);
+        for (int r = 0; r < p.b_rows; r += p.b_box_rows)
+          for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
+            tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
+      }
       pdl_wait();  // X / W may be produced by the preceding kernel
       const uint32_t slab_tx = static_cast<uint32_t>(p.HR) * p.Wv * 128;
       uint32_t slot = 0, phase = 0;

@@ -393,6 +393,18 @@ __device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float
   mc_cluster_sync();  // peers have finished reading this CTA's partial
 }
 
+// Debug timeline (p.trace only; tools/floor_timeline.py): %globaltimer (ns) of
+// kernel milestones of CTA b < 256 at trace[8192 + 8 * b + event].
+enum TraceEvent { TR_ENTRY = 0, TR_PDL_DONE = 1, TR_FIRST_FULL = 2, TR_FIRST_TFULL = 3, TR_STORES_DONE = 4,
+                  TR_EXIT = 5 };
+__device__ __forceinline__ void trace_event(unsigned long long* trace, int ev) {
+  if (trace && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    trace[8192 + 8 * blockIdx.x + ev] = t;
+  }
+}
+
 // Piece table entry: everything a producer needs for one TMA piece, computed
 // once per launch so the producer loop does no index arithmetic.
 //   x = channel offset within the group (cb * box)
@@ -425,6 +437,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
+  if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
   const int S = p.stages;
   const bool b_res = p.b_mode == B_RESIDENT;
   constexpr int kBSlotBytes = CG2 ? Cfg::kBBytes / 2 : Cfg::kBBytes;  // cg2: this CTA's half of B
@@ -505,6 +518,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   if (warp >= kEpi && warp < kEpi + kProducers) {
     // ------------------------------------------------------------ producers
     pdl_wait();  // operands may be produced by the preceding kernel
+    if (warp == kEpi && lane == 0) trace_event(p.trace, TR_PDL_DONE);
     // Every producer walks every stage and issues a round-robin share of its
     // TMA requests (pieces j = pw mod 4; B chunks after them), arriving on the
     // stage's full barrier with its own expect_tx. A single issuing thread
@@ -703,6 +717,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       for (int st = st0; st < st1; ++st, ++it) {
         mbar_wait(&full[slot], phase);
         tc_fence_after();
+        if (it == 0 && lane == 0) trace_event(p.trace, TR_FIRST_FULL);
         if (trace && lane == 0 && it < 128) trace[256 + 2 * it] = clock64();
         const uint64_t a = adesc0 + slot * kAslot;
         const uint64_t b = bdesc0 + (b_res ? st * kBst : slot * kBslot);
@@ -816,6 +831,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         fetch_res(c_first);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (local == 0 && threadIdx.x == 0) trace_event(p.trace, TR_FIRST_TFULL);
         if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
 #pragma unroll 1
         for (int c0 = c_first; c0 < BN; c0 += kHs * cw, ++chunk) {
@@ -925,6 +941,10 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         }
       }
       if (lane == 0) tma_store_wait_read<0>();  // smem reads done; the grid end flushes the writes
+      if (threadIdx.x == 0 && p.trace) {
+        tma_store_wait_all<0>();  // (trace only) the stores themselves complete
+        trace_event(p.trace, TR_STORES_DONE);
+      }
     } else {
       // Generic: TMEM -> registers (thread = output row) -> smem transpose ->
       // coalesced stores of 32-column row segments at per-row output offsets
@@ -1058,6 +1078,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     else
       tmem_dealloc(tmem_base, Cfg::kTmemCols);
   }
+  if (threadIdx.x == 0) trace_event(p.trace, TR_EXIT);
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
     uint64_t t_end;
     uint32_t smid;

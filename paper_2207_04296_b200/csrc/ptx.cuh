@@ -92,6 +92,23 @@ __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");
 }
 
+// L2 prefetches of TMA boxes (no shared memory, no barrier). Issued BEFORE
+// griddepcontrol.wait for a kernel's first loads: L2 is the point of coherence
+// for global memory, so a line prefetched while the preceding kernel still
+// writes it is updated in place by those writes — the prefetch only moves the
+// DRAM latency of the first tile under the previous kernel's tail, it never
+// lets stale data through (the real loads still come after the wait).
+__device__ __forceinline__ void tma_prefetch_2d(const CUtensorMap* m, int c0, int c1) {
+  asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(m), "r"(c0), "r"(c1)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_prefetch_4d(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(m), "r"(c0),
+               "r"(c1), "r"(c2), "r"(c3)
+               : "memory");
+}
+
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0,
                                             int c1) {
   asm volatile(

@@ -825,6 +825,7 @@ int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
   int grid = std::min(p.total_tiles, di.sms / keys * keys);
   if (const int e = tb::options().max_ctas) grid = std::max(1, std::min(grid, e));
   p.trace = g_trace;
+  p.l2_prefetch = tb::options().l2_prefetch;
   CUDA_TRY(launch_pdl(tb::conv_halo_kernel<BN, KH, KW>, grid, tb::kHaloThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
