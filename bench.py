@@ -222,7 +222,7 @@ class OpRunner:
         if is_gmm(name):
             M, N, K = gmm_shape(name)
             set_bytes = M * K * 2 + K * N * 2 + M * N * 4
-            self.sets = min(max(2, math.ceil(2 * L2_BYTES / set_bytes)), 32)
+            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
             self.A = [torch.randn(M, K, device=device, generator=g).half() for _ in range(self.sets)]
             self.B = [torch.randn(K, N, device=device, generator=g).half() for _ in range(self.sets)]
             self.C = [torch.empty(M, N, device=device) for _ in range(self.sets)]
@@ -231,14 +231,14 @@ class OpRunner:
             spec = op_spec(name)
             self.spec = spec
             xs, ws, ys = spec.x_shape(), spec.w_shape(), spec.y_shape()
-            n_x = math.prod(xs) * 2
-            n_y = math.prod(ys) * 4
-            self.sets = max(2, math.ceil(2 * L2_BYTES / (n_x + n_y)))
-            self.sets = min(self.sets, 64)
+            # every operand rotates (weights too: T2D's 4.2 MB weight panel would
+            # otherwise stay L2-resident), > 2x L2 in total
+            set_bytes = (math.prod(xs) + math.prod(ws)) * 2 + math.prod(ys) * 4
+            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
             self.X = [torch.randn(*xs, device=device, generator=g).half() for _ in range(self.sets)]
-            self.W = torch.randn(*ws, device=device, generator=g).half()
+            self.W = [torch.randn(*ws, device=device, generator=g).half() for _ in range(self.sets)]
             self.Y = [torch.empty(*ys, device=device) for _ in range(self.sets)]
-            self.fn = lambda i: tb.conv(spec, self.X[i], self.W, self.Y[i])
+            self.fn = lambda i: tb.conv(spec, self.X[i], self.W[i], self.Y[i])
 
     def step(self, i):
         self.fn(i % self.sets)
@@ -386,12 +386,17 @@ def measure_e2e_interp(name, runs=3):
                        "interpreter's input and output tensors"}
 
 
+TRAFFIC_PROFILE = "r02_ncu_graph_traffic.json"
+
+
 def traffic_from_profiles(name):
-    """dram read+write bytes per launch from the committed ncu --set full summary."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    """Steady-state DRAM read + write bytes per launch of this op, from the committed
+    ncu capture of a CUDA graph of consecutive launches on rotating buffers
+    (profiles/r02_ncu_graph_traffic.json, tools/ncu_graph_summary.py)."""
+    p = os.path.join(ROOT, "profiles", TRAFFIC_PROFILE)
     try:
         with open(p) as f:
-            return json.load(f).get(name)
+            return json.load(f)["ops"][name]["traffic_per_launch"]
     except Exception:
         return None
 
@@ -540,8 +545,8 @@ def main():
     ap.add_argument("--nets", default="resnet50,mobilenet_v2,bert_large")
     ap.add_argument("--profile", metavar="OP", help="eager launches of one op for ncu (no timing)")
     ap.add_argument("--profile-range", metavar="OP",
-                    help="warm-up, then --steps launches of one op between cudaProfilerStart/Stop "
-                         "(ncu --replay-mode range: steady-state DRAM bytes and time per launch)")
+                    help="a CUDA graph of --steps launches of one op, replayed between cudaProfilerStart/Stop "
+                         "(ncu --graph-profiling graph: steady-state DRAM bytes and time per launch)")
     ap.add_argument("--launcher-check", action="store_true",
                     help="rank bookkeeping only (gloo, no GPU): one JSON line with the ranks seen")
     args = ap.parse_args()
@@ -572,13 +577,22 @@ def main():
     if args.profile_range:
         import torch
 
+        # the K launches are captured into one CUDA graph (tensor maps are encoded at
+        # capture), and only its replay lies between cudaProfilerStart / Stop:
+        # `ncu --graph-profiling graph --profile-from-start off` then reports the
+        # whole graph as one result (DRAM bytes incl. write-backs, total time)
         r = OpRunner(args.profile_range, torch.device("cuda", 0))
         for i in range(args.warmup):
             r.step(i)
         torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, capture_error_mode="relaxed"):
+            for i in range(args.steps):
+                r.step(args.warmup + i)
+        g.replay()
+        torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()
-        for i in range(args.steps):
-            r.step(args.warmup + i)
+        g.replay()
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStop()
         return

@@ -355,3 +355,86 @@ extern "C" int tir_b200_adapter_time_run(const char* ir_text, const char* block,
     }
   });
 }
+
+// SURVEY §8(c) per-intrinsic oracle: the same tensorized program run with the
+// reference's OWN scalar implementation of the intrinsic — make_scalar_kernel
+// (src/interp.cc:594-726) built from a description PrimFunc `desc_text` (its
+// compute block's body, iterated over the block domain; no init: accumulate
+// semantics) — registered under the intrinsic's name instead of the B200
+// kernel. `params_csv` names the description params in view order
+// ("C,A,B": writes[0] first, then reads, interp.cc:371-373).
+extern "C" int tir_b200_adapter_run_scalar(const char* ir_text, const char* intrin, const char* desc_text,
+                                           const char* params_csv, int n_in, const float* const* inputs, float* out,
+                                           int64_t out_elems, int64_t* intrinsic_calls, char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    std::vector<std::string> params;
+    std::string cur;
+    for (const char* c = params_csv; *c; ++c) {
+      if (*c == ',') {
+        params.push_back(cur);
+        cur.clear();
+      } else {
+        cur += *c;
+      }
+    }
+    if (!cur.empty()) params.push_back(cur);
+    tir::PrimFuncPtr f = tir::parse_text(ir_text);
+    tir::ExecContext ctx;
+    ctx.register_host_kernel(intrin, tir::make_scalar_kernel(tir::parse_text(desc_text), params));
+    run_program(*f, ctx, n_in, inputs, out, out_elems, intrinsic_calls);
+  });
+}
+
+namespace {
+
+// Names of the views a tensorized block hands its kernel: writes[0], then reads.
+std::vector<std::string> operand_names(const tir::PrimFunc& f, const std::string& intrin) {
+  std::vector<std::string> names;
+  tir::pre_order_stmts(f.body, [&](const tir::Stmt& s) {
+    if (s->kind == tir::StmtKind::BlockRealize && s->block) {
+      auto it = s->block->annotations.find("tensorized");
+      if (it != s->block->annotations.end() && it->second == intrin && names.empty()) {
+        names.push_back(s->block->writes.at(0).buffer->name);
+        for (const auto& r : s->block->reads) names.push_back(r.buffer->name);
+      }
+    }
+    return names.empty();
+  });
+  return names;
+}
+
+}  // namespace
+
+// Tensorize `block`, then emit a program in the reference grammar: the `intrin`
+// declaration of the generated intrinsic (tir_b200_tensorize.h intrin_decl_text)
+// followed by the tensorized function. The text is checked to parse back with
+// tir::parse_program (one function, one declaration with one constraint per
+// view) before it is returned.
+extern "C" int tir_b200_adapter_declare(const char* ir_text, const char* block, char* program, int64_t program_len,
+                                        char* err, int errlen) {
+  return guarded(err, errlen, [&] {
+    tir::Schedule s(tir::parse_text(ir_text));
+    const tir_b200::OpMatch m = tir_b200::tensorize_whole_op(s, block);
+    const auto ops = operand_names(*s.func(), m.intrin);
+    const std::string text = tir_b200::intrin_decl_text(m, ops) + "\n" + tir::print_text(s.func());
+    tir::ParsedProgram pp = tir::parse_program(text);
+    if (pp.funcs.size() != 1 || pp.intrins.size() != 1 || pp.intrins[0].name != m.intrin ||
+        pp.intrins[0].constraints.size() != ops.size())
+      tir::throw_error("InternalError", "declaration does not round-trip through parse_program");
+    copy_out(text, program, program_len, "program");
+  });
+}
+
+// Run a program whose b200.* intrinsics are registered from its own `intrin`
+// declarations (register_declared): no other registration step.
+extern "C" int tir_b200_adapter_run_declared(const char* program_text, int n_in, const float* const* inputs,
+                                             float* out, int64_t out_elems, int64_t* intrinsic_calls, char* err,
+                                             int errlen) {
+  return guarded(err, errlen, [&] {
+    tir::ParsedProgram pp = tir::parse_program(program_text);
+    if (pp.funcs.empty()) tir::throw_error("ValueError", "program has no function");
+    tir::ExecContext ctx;
+    if (tir_b200::register_declared(ctx, pp) == 0) tir::throw_error("ValueError", "no b200 intrinsic declared");
+    run_program(*pp.funcs[0], ctx, n_in, inputs, out, out_elems, intrinsic_calls);
+  });
+}

@@ -1,6 +1,9 @@
 // tir_b200_tensorize.cc — whole-op tensorize composite (see the header).
 #include "tir_b200_tensorize.h"
 
+#include <cstdio>
+#include <cstring>
+
 #include <algorithm>
 #include <map>
 #include <set>
@@ -453,6 +456,70 @@ OpMatch tensorize_whole_op(tir::Schedule& s, const std::string& block) {
   replace_with_call(trial, outer, m.intrin, m.overwrite);
   s = trial;
   return m;
+}
+
+std::string intrin_decl_text(const OpMatch& m, const std::vector<std::string>& operands) {
+  std::string t = "intrin " + m.intrin + " {\n";
+  for (const auto& o : operands) t += "  require " + o + " scope(\"global\") contiguous\n";
+  return t + "}\n";
+}
+
+OpMatch decode_intrin(const std::string& name) {
+  OpMatch m;
+  std::string key = name;
+  if (key.size() > 3 && key.compare(key.size() - 3, 3, ".ow") == 0) {
+    m.overwrite = true;
+    key.resize(key.size() - 3);
+  }
+  m.intrin = name;
+  if (key == "b200.gmm") {
+    m.gmm = true;
+    return m;
+  }
+  static const char* tags[] = {"gmm", "c1d", "c2d", "c3d", "dil", "grp", "t2d", "dep"};
+  tir_b200_conv_desc d{};
+  char tag[8] = {0};
+  long long v[20];
+  const int got = std::sscanf(key.c_str(),
+                              "b200.%7[a-z0-9].n%lld_i%lldx%lldx%lld_c%lld_o%lld_k%lldx%lldx%lld_s%lldx%lldx%lld_p%lldx%lldx"
+                              "%lld_d%lldx%lldx%lld_g%lld",
+                              tag, &v[0], &v[1], &v[2], &v[3], &v[4], &v[5], &v[6], &v[7], &v[8], &v[9], &v[10],
+                              &v[11], &v[12], &v[13], &v[14], &v[15], &v[16], &v[17], &v[18]);
+  if (got != 20) tir::throw_error("DescMismatch", "'" + name + "' is not a b200 intrinsic name");
+  d.op = -1;
+  for (int i = 0; i < 8; ++i)
+    if (!std::strcmp(tag, tags[i])) d.op = i;
+  if (d.op <= 0) tir::throw_error("DescMismatch", "'" + name + "': unknown operator tag");
+  d.transposed = d.op == TIR_B200_T2D;
+  d.n = v[0];
+  d.in_d = v[1]; d.in_h = v[2]; d.in_w = v[3];
+  d.ci = v[4]; d.co = v[5];
+  d.k_d = v[6]; d.k_h = v[7]; d.k_w = v[8];
+  d.s_d = v[9]; d.s_h = v[10]; d.s_w = v[11];
+  d.p_d = v[12]; d.p_h = v[13]; d.p_w = v[14];
+  d.d_d = v[15]; d.d_h = v[16]; d.d_w = v[17];
+  d.groups = v[18];
+  if (conv_intrin_key(d) != key) tir::throw_error("DescMismatch", "'" + name + "' does not round-trip");
+  int64_t out[3];
+  if (tir_b200_conv_out_shape(&d, out) != TIR_B200_OK)
+    tir::throw_error("DescMismatch", "'" + name + "': " + tir_b200_last_error());
+  m.conv = d;
+  return m;
+}
+
+int register_declared(tir::ExecContext& ctx, const tir::ParsedProgram& program) {
+  int n = 0;
+  for (const auto& decl : program.intrins) {
+    if (decl.name.rfind("b200.", 0) != 0) continue;  // someone else's intrinsic
+    if (!decl.exec_scope.empty())
+      tir::throw_error("DescMismatch", decl.name + ": B200 whole-op intrinsics take no exec_scope");
+    for (const auto& [param, c] : decl.constraints)
+      if (!c.scope.empty() && c.scope != "global")
+        tir::throw_error("DescMismatch", decl.name + ": operand " + param + " must be in global scope");
+    register_matched(ctx, decode_intrin(decl.name));
+    ++n;
+  }
+  return n;
 }
 
 void register_matched(tir::ExecContext& ctx, const OpMatch& m) {

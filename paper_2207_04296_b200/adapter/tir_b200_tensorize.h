@@ -31,6 +31,7 @@
 
 #include "tir/interp.h"
 #include "tir/schedule.h"
+#include "tir/text.h"
 #include "tir_b200.h"
 
 namespace tir_b200 {
@@ -73,6 +74,22 @@ int64_t pad_conv_channels(tir::Schedule& s, const std::string& block, int64_t mu
 
 // Full-geometry intrinsic name, e.g. "b200.c2d.n16_i1x56x56_c64_o64_k1x3x3_s1x1x1_p0x1x1_d1x1x1_g1".
 std::string conv_intrin_key(const tir_b200_conv_desc& d);
+
+// Intrinsic declarations in the reference grammar (`intrin NAME { require P
+// scope("global") contiguous ... }`, parser.cc:749-781, text.h:45-59).
+// intrin_decl_text emits the declaration of a matched intrinsic: its operands
+// (views [writes[0], reads...], named after the block's buffers) must be
+// global, row-major, innermost-contiguous — what the C-ABI consumes — and, as
+// whole-op blocks must, it carries no exec_scope (TH-SCOPE, validate.cc:432-455).
+// register_declared builds the B200 HostKernel registry from a parsed program
+// alone: the full geometry is in the intrinsic name (conv_intrin_key, plus
+// ".ow" for the overwriting form), so each `b200.*` declaration is decoded and
+// registered; a declaration asking for anything else (another scope, an
+// exec_scope, an undecodable name) throws DescMismatch. Returns the count.
+std::string intrin_decl_text(const OpMatch& m, const std::vector<std::string>& operands);
+int register_declared(tir::ExecContext& ctx, const tir::ParsedProgram& program);
+// Decodes an intrinsic name produced by tensorize_whole_op (inverse of conv_intrin_key).
+OpMatch decode_intrin(const std::string& name);
 
 }  // namespace tir_b200
 

@@ -216,3 +216,67 @@ def test_epilogue_program_with_tensorized_conv(cuda):
     out, calls = run_auto(src, ["conv"], [x, w, bias], spec.y_shape())
     assert calls == 1
     assert O.tensors_bitwise_equal(out, O.epilogue(O.conv(spec, x, w), bias, True))
+
+
+def declare(ir: str, block: str) -> str:
+    L = adapter()
+    L.tir_b200_adapter_declare.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64,
+                                           ctypes.c_char_p, ctypes.c_int]
+    out = ctypes.create_string_buffer(1 << 20)
+    err = ctypes.create_string_buffer(2048)
+    if L.tir_b200_adapter_declare(ir.encode(), block.encode(), out, len(out), err, len(err)) != 0:
+        _raise(err)
+    return out.value.decode()
+
+
+def run_declared(program: str, inputs, out_shape):
+    L = adapter()
+    f32p = ctypes.POINTER(ctypes.c_float)
+    L.tir_b200_adapter_run_declared.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(f32p), f32p,
+                                                ctypes.c_int64, ctypes.POINTER(ctypes.c_int64), ctypes.c_char_p,
+                                                ctypes.c_int]
+    ins = [np.ascontiguousarray(x, np.float32) for x in inputs]
+    arr = (f32p * len(ins))(*[x.ctypes.data_as(f32p) for x in ins])
+    out = np.zeros(out_shape, np.float32)
+    calls = ctypes.c_int64(0)
+    err = ctypes.create_string_buffer(2048)
+    if L.tir_b200_adapter_run_declared(program.encode(), len(ins), arr, out.ctypes.data_as(f32p), out.size,
+                                       ctypes.byref(calls), err, len(err)) != 0:
+        _raise(err)
+    return out, calls.value
+
+
+@pytest.mark.parametrize("name", ["C2D", "T2D", "DEP", "C3D"])
+def test_intrin_declaration_round_trips(name):
+    """the tensorized program carries an `intrin` declaration
+    of its B200 intrinsic in the reference grammar (parser.cc:749-781): one
+    `require <view> scope("global") contiguous` per view ([writes[0], reads...]),
+    no exec_scope; it parses back with tir::parse_program (checked inside)."""
+    prog = declare(G.conv_source(SPECS[name]), "conv")
+    head = prog.split("\n\n")[0]
+    assert head.startswith("intrin b200.") and ".ow {" in head
+    assert head.count('scope("global") contiguous') == 3 and "exec_scope" not in head
+    assert "func " in prog and "tensorized" in prog
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP"])
+def test_registry_from_declarations_runs_bit_exact(name, cuda):
+    """The kernel registry built from the program's own declarations
+    (register_declared decodes the full geometry from the intrinsic name):
+    tir::run of the declared program is bit-exact vs the oracle."""
+    spec = SPECS[name]
+    x = O.reference_tensor(spec.x_shape(), 1)
+    w = O.reference_tensor(spec.w_shape(), 2)
+    out, calls = run_declared(declare(G.conv_source(spec), "conv"), [x, w], spec.y_shape())
+    assert calls == 1
+    assert O.tensors_bitwise_equal(out, O.conv(spec, x, w))
+
+
+def test_declarations_reject_foreign_requirements():
+    prog = declare(G.conv_source(SPECS["C2D"]), "conv")
+    bad = prog.replace('scope("global")', 'scope("shared")', 1)
+    with pytest.raises(api.TirError) as e:
+        run_declared(bad, [np.zeros(SPECS["C2D"].x_shape(), np.float32),
+                           np.zeros(SPECS["C2D"].w_shape(), np.float32)], SPECS["C2D"].y_shape())
+    assert e.value.kind == "DescMismatch"
