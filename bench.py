@@ -586,9 +586,11 @@ def main():
             r.step(i)
         torch.cuda.synchronize()
         g = torch.cuda.CUDAGraph()
+        steps = max(args.steps, r.sets)  # every rotating set once: the graph's data exceeds 2x L2
         with torch.cuda.graph(g, capture_error_mode="relaxed"):
-            for i in range(args.steps):
+            for i in range(steps):
                 r.step(args.warmup + i)
+        print(json.dumps({"profile_range": args.profile_range, "launches": steps, "sets": r.sets}), flush=True)
         g.replay()
         torch.cuda.synchronize()
         torch.cuda.cudart().cudaProfilerStart()

@@ -94,6 +94,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   uint64_t* bfull = tempty + Cfg::kNacc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
+  if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
   const uint32_t warp = warp_id(), lane = lane_id();
   if (threadIdx.x == 32 * 8 + 1) {  // descriptor fetches overlap the prologue
     prefetch_tmap(&p.tmX);
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
             tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
       }
       pdl_wait();  // X / W may be produced by the preceding kernel
+      trace_event(p.trace, TR_PDL_DONE);
       const uint32_t slab_tx = static_cast<uint32_t>(p.HR) * p.Wv * 128;
       uint32_t slot = 0, phase = 0;
       int it = 0;
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
       if (i % p.cblocks == 0) mbar_wait(&tempty[ac], acph ^ 1);
       mbar_wait(&full[sl], ph);
       tc_fence_after();
+      if (i == 0 && lane == 0) trace_event(p.trace, TR_FIRST_FULL);
     };
     if (nstage > 0) wait_stage(0, 0, 0, 0, 0);
     for (int i = 0; i < nstage; ++i) {
@@ -306,6 +309,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
         fetch_res(0);
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (threadIdx.x == 0 && tile == static_cast<int>(blockIdx.x)) trace_event(p.trace, TR_FIRST_TFULL);
         if (trace && threadIdx.x == 0) trace[512 + 2 * (tile / gridDim.x)] = clock64();
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32, ++chunk) {
@@ -389,7 +393,10 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
           acc_phase ^= 1;
         }
       }
-      if (threadIdx.x == 0) tma_store_wait_all<0>();
+      if (threadIdx.x == 0) {
+        tma_store_wait_all<0>();
+        trace_event(p.trace, TR_STORES_DONE);
+      }
     }
   } else {
     // ------------------------------------------------------------ epilogue (warps 0-7)
@@ -482,6 +489,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
   __syncthreads();
   tc_fence_after();
   if (warp == 9) tmem_dealloc(tmem_base, Cfg::kTmemCols);
+  if (threadIdx.x == 0) trace_event(p.trace, TR_EXIT);
   if (p.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
     uint64_t t_end;
     uint32_t smid;

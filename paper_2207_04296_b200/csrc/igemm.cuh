@@ -390,19 +390,8 @@ __device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float
       }
     }
   }
+  if (threadIdx.x == 0) trace_event(p.trace, TR_STORES_DONE);
   mc_cluster_sync();  // peers have finished reading this CTA's partial
-}
-
-// Debug timeline (p.trace only; tools/floor_timeline.py): %globaltimer (ns) of
-// kernel milestones of CTA b < 256 at trace[8192 + 8 * b + event].
-enum TraceEvent { TR_ENTRY = 0, TR_PDL_DONE = 1, TR_FIRST_FULL = 2, TR_FIRST_TFULL = 3, TR_STORES_DONE = 4,
-                  TR_EXIT = 5 };
-__device__ __forceinline__ void trace_event(unsigned long long* trace, int ev) {
-  if (trace && blockIdx.x < 256) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    trace[8192 + 8 * blockIdx.x + ev] = t;
-  }
 }
 
 // Piece table entry: everything a producer needs for one TMA piece, computed
@@ -770,6 +759,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
+        if (threadIdx.x == 0) trace_event(p.trace, TR_FIRST_TFULL);
 #pragma unroll 1
         for (int c0 = static_cast<int>(hh) * kChunk; c0 < BN; c0 += kHs * kChunk) {
           uint32_t r[32];
@@ -980,6 +970,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
         if (trace && threadIdx.x == 0 && local < 64) trace[512 + 2 * local] = clock64();
+        if (local == 0 && threadIdx.x == 0) trace_event(p.trace, TR_FIRST_TFULL);
         const int ncol0 = nt * BN;
         constexpr int kChunk = BN < 32 ? BN : 32;
         constexpr int kLanesPerRow = kChunk / 4;

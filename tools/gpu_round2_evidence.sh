@@ -16,6 +16,8 @@ for op in ${OPS:-C2D GMM C1D GRP T2D DEP DIL C3D DEP_112c96s2 DEP_56c144s1 GMM8K
   timeout 600 ncu --graph-profiling graph --profile-from-start off --cache-control none --clock-control none \
       --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum --csv \
       python bench.py --profile-range $op --steps $steps --warmup 3 > gpurun_out/r02/range_$op.csv 2> gpurun_out/r02/range_$op.err
-  echo "$op rc=$? steps=$steps" >> gpurun_out/r02/range_steps.txt
+  rc=$?
+  steps=$(grep -o '"launches": [0-9]*' gpurun_out/r02/range_$op.csv | grep -o '[0-9]*$')
+  echo "$op rc=$rc steps=$steps" >> gpurun_out/r02/range_steps.txt
 done
 tail -3 gpurun_out/r02/range_C2D.csv
