@@ -222,7 +222,7 @@ class OpRunner:
         if is_gmm(name):
             M, N, K = gmm_shape(name)
             set_bytes = M * K * 2 + K * N * 2 + M * N * 4
-            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
+            self.sets = int(os.environ.get("BENCH_DIAG_SETS", 0)) or max(2, math.ceil(2 * L2_BYTES / set_bytes))
             self.A = [torch.randn(M, K, device=device, generator=g).half() for _ in range(self.sets)]
             self.B = [torch.randn(K, N, device=device, generator=g).half() for _ in range(self.sets)]
             self.C = [torch.empty(M, N, device=device) for _ in range(self.sets)]
@@ -234,7 +234,8 @@ class OpRunner:
             # every operand rotates (weights too: T2D's 4.2 MB weight panel would
             # otherwise stay L2-resident), > 2x L2 in total
             set_bytes = (math.prod(xs) + math.prod(ws)) * 2 + math.prod(ys) * 4
-            self.sets = max(2, math.ceil(2 * L2_BYTES / set_bytes))
+            # BENCH_DIAG_SETS (diagnostics only, e.g. tools/cta_timeline.py): a fixed set count
+            self.sets = int(os.environ.get("BENCH_DIAG_SETS", 0)) or max(2, math.ceil(2 * L2_BYTES / set_bytes))
             self.X = [torch.randn(*xs, device=device, generator=g).half() for _ in range(self.sets)]
             self.W = [torch.randn(*ws, device=device, generator=g).half() for _ in range(self.sets)]
             self.Y = [torch.empty(*ys, device=device) for _ in range(self.sets)]

@@ -150,9 +150,15 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
         decompose(blockIdx.x, n, th, tw, g, nt);
         for (int cb = 0; cb < p.cblocks && cb < S; ++cb)
           tma_prefetch_4d(&p.tmX, g * p.cig + cb * 64, tw * p.Wt - p.pad_w, th * p.R - p.pad_h, n);
+        // The weight panel is shared by every CTA of the (group, n-tile): each CTA
+        // prefetches one box of it (l2_prefetch == 2; 1 = every box, measured
+        // 0.4 us slower: an SM's TMA unit works through its prefetches in order,
+        // ahead of the first real load).
+        int box = 0;
         for (int r = 0; r < p.b_rows; r += p.b_box_rows)
-          for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch)
-            tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
+          for (int ch = 0; ch < BN / Cfg::kBChunk; ++ch, ++box)
+            if (p.l2_prefetch == 1 || box == static_cast<int>(blockIdx.x) / (p.groups * p.tiles_n))
+              tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
       }
       pdl_wait();  // X / W may be produced by the preceding kernel
       trace_event(p.trace, TR_PDL_DONE);
@@ -208,6 +214,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
     if (static_cast<int>(blockIdx.x) < p.total_tiles) {
       mbar_wait(bfull, 0);
       tc_fence_after();
+      if (trace && lane == 0) trace[1022] = clock64();
     }
     // Flattened stage loop (stage = (tile, channel block)). The barriers of
     // stage i+1 are waited on after all but the last tap of stage i is issued,
@@ -388,6 +395,7 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
+        if (trace && threadIdx.x == 0) trace[513 + 2 * (tile / gridDim.x)] = clock64();
         if (++acc == static_cast<uint32_t>(Cfg::kNacc)) {
           acc = 0;
           acc_phase ^= 1;

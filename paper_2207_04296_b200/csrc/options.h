@@ -33,8 +33,8 @@ struct Options {
   int dep_tc = 0;          // 8 / 16: DEP stride-1 tile-width override
   int no_smem_bias = 0;    // 1: never stage the bias in shared memory
   int host_pipeline = 1;   // 0: host-buffer calls do not pipeline batch chunks
-  int l2_prefetch = 1;     // 0: the halo conv does not prefetch its first tile into L2 before the PDL
-                           // wait (measured: the same prefetch in igemm / DEP cost 0.7-1.7 us — the
+  int l2_prefetch = 2;     // 0: the halo conv does not prefetch its first tile into L2 before the PDL
+                           // wait; 1: it also prefetches the whole weight panel (2: one box per CTA) (measured: the same prefetch in igemm / DEP cost 0.7-1.7 us — the
                            // prefetches occupy the TMA queue ahead of the real loads — so only halo has it)
 };
 
