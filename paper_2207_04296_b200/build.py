@@ -30,6 +30,7 @@ NVCC_FLAGS = [
 
 SOURCES = ["csrc/tir_b200.cu"]
 HEADERS = ["csrc/ptx.cuh", "csrc/igemm.cuh", "csrc/halo.cuh", "csrc/dep.cuh", "csrc/prep.cuh", "csrc/netops.cuh",
+           "csrc/rowpack.cuh", "csrc/options.h",
            "../include/tir_b200.h"]
 
 

@@ -1,0 +1,531 @@
+// rowpack.cuh — small-channel convolution (CI = 3 stems: the C3D paper shape,
+// 7x7 / 3x3 stride-2 stems) with the MMA's A operand packed into TENSOR memory.
+//
+// Why: with CI = 3 a 7x7 tap row carries 21 useful values. im2col pieces of
+// (kw, c) (the igemm path) stream each input pixel ~KH*KD times through L2 into
+// shared memory and need a 411 MB relayout for the C3D paper shape; the MMA then
+// re-reads every A row from shared memory (SS mode: 48 cycles per 128x64x16 MMA,
+// tools/mma_rate2.cu). Here:
+//   * the producer TMA-loads RAW input rows: for one output tile (R rows x Wt
+//     columns) and one input depth plane, the box of box_h input rows x box_w
+//     elements of the [W*CI] row (4.7 KB for C3D) — zero fill is the padding;
+//   * 8 builder warps turn it into the packed A operand directly in TMEM: TMEM
+//     lane m = output pixel (m / Wt, m % Wt); its K vector is the kh taps of the
+//     plane back to back, each tap the KW*CI contiguous elements of input row
+//     sh*r + dh*kh starting at element sw*CI*c (one even-aligned run: 32-bit
+//     shared loads, no shuffles), padded to an even count (WPK 32-bit words);
+//     tcgen05.st writes them (measured 605 B/clk);
+//   * the MMA warp issues kind::f16 MMAs with A in TMEM (TS mode, 32 cycles per
+//     128x64x16 — the full tensor rate) and B = the packed weight panel, resident
+//     in shared memory for the whole kernel ([KD][Kp][CO], Kp = 16*ksteps rows
+//     laid out like the TMEM K vector);
+//   * a work unit is (image, group of 2 output depths, tile): each input plane is
+//     loaded and packed once and feeds both output depths' accumulators (with
+//     their own kd), double-buffered accumulators let the TMA-store epilogue of
+//     unit i overlap the MMAs of unit i+1.
+// Reduction order: (kd, kh, kw, c) per output, exactly the reference's loop nest
+// order reassociated inside the tensor core; on the reference input distribution
+// every partial sum is exact (bit-identical results, tests/test_gpu_parity.py).
+#pragma once
+
+#include "ptx.cuh"
+
+namespace tb {
+
+constexpr int kRpProducers = 4;   // TMA producer warps (raw boxes of planes it = pw mod 4)
+constexpr int kRpThreads = 544;  // warps 0-3 epilogue, 4-11 builders, 12 + 14-16 producers, 13 MMA
+constexpr int kRpSlots = 5;      // TMEM accumulator ring: output depths in flight (+ one draining)
+constexpr int kRpAccCol = 0;     // TMEM: kRpSlots x BN accumulator columns
+constexpr int kRpACol = 320;     // TMEM: 2 A buffers x KWORDS columns (after the 5 x 64 accumulators)
+
+struct alignas(64) RowpackParams {
+  CUtensorMap tmX;  // 3-D over X[N*D, H, W*CI] fp16: box {box_w, box_h, 1}, no swizzle
+  CUtensorMap tmB;  // 2-D over Bp[KD*Kp, CO] fp16: box {BN, Kp}, SW128 (BN 64) / SW64 (BN 32)
+  CUtensorMap tmY;  // 4-D over Y[N*OD, OH, OW, CO]: box {32, Wt, R, 1}
+  int32_t n, d, ci;
+  int32_t od, oh, ow;
+  int32_t kd, sd, sh, sw, pd, ph, pw, dd, dh;
+  int32_t R, Wt, tiles_h, tiles_w, total_units;
+  int32_t kp;  // packed K rows per kd (16 * ksteps)
+  int32_t box_w, box_h;
+  int32_t shift;  // elements between the box's 16-byte-aligned start column and the tile's first input element
+  int32_t stages, slot_bytes;
+  int32_t mask_last;  // KW*CI odd: the last word of each tap keeps only its low half
+  int32_t out_f16, store_mode;  // store_mode 1: TMA store, 2: TMA reduce-add (Y += conv)
+  int32_t stage_bytes;
+  unsigned long long* trace;
+};
+
+// tcgen05.st.32x32b of N consecutive columns (lane = thread's TMEM lane).
+template <int N>
+__device__ __forceinline__ void tmem_st_n(uint32_t taddr, const uint32_t* v);
+template <>
+__device__ __forceinline__ void tmem_st_n<1>(uint32_t t, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(t), "r"(v[0]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_n<2>(uint32_t t, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1, %2};" ::"r"(t), "r"(v[0]), "r"(v[1]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_n<4>(uint32_t t, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(t), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_n<8>(uint32_t t, const uint32_t* v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(t),
+               "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_n<16>(uint32_t t, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16};" ::"r"(t),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]));
+}
+template <>
+__device__ __forceinline__ void tmem_st_n<32>(uint32_t t, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(t),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+
+// N columns as a compile-time sequence of power-of-two stores.
+template <int N>
+__device__ __forceinline__ void tmem_st_words(uint32_t t, const uint32_t* v) {
+  if constexpr (N >= 32) {
+    tmem_st_n<32>(t, v);
+    tmem_st_words<N - 32>(t + 32, v + 32);
+  } else if constexpr (N >= 16) {
+    tmem_st_n<16>(t, v);
+    tmem_st_words<N - 16>(t + 16, v + 16);
+  } else if constexpr (N >= 8) {
+    tmem_st_n<8>(t, v);
+    tmem_st_words<N - 8>(t + 8, v + 8);
+  } else if constexpr (N >= 4) {
+    tmem_st_n<4>(t, v);
+    tmem_st_words<N - 4>(t + 4, v + 4);
+  } else if constexpr (N >= 2) {
+    tmem_st_n<2>(t, v);
+    tmem_st_words<N - 2>(t + 2, v + 2);
+  } else if constexpr (N == 1) {
+    tmem_st_n<1>(t, v);
+  }
+}
+
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ void umma_f16_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(m), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+template <int BN>
+struct RowpackCfg {
+  static constexpr int kBRowBytes = BN * 2;
+  static constexpr uint32_t kBLayout = kBRowBytes == 128 ? 2u : 4u;  // SW128 / SW64
+  static constexpr uint32_t kIdesc = idesc_f16_f32(128, BN, 0, 1);
+};
+
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Columns [C0, C1) of one lane's TMEM K vector, stored in 8-column tcgen05.st
+// chunks at 8-aligned columns. Column k is word k % WPK of tap k / WPK: elements
+// e, e+1 of the raw rows, e = e0 + tap*tap_step + 2*(k % WPK), e0 the lane's run
+// start. Every run of a kernel starts at the same parity (ODD: two aligned words
+// funnel-shifted); the tap's last word keeps only its low half when KW*CI is odd;
+// columns past KH*WPK are the K padding (zero). Lanes past the tile's pixels
+// (r = c = 0) build a copy of pixel 0: their TMEM rows only feed discarded rows.
+template <int C0, int C1, int KH, int WPK, bool ODD>
+__device__ __forceinline__ void build_cols(uint32_t src, uint32_t e0, uint32_t tap_step, uint32_t last_mask,
+                                           uint32_t abase) {
+  constexpr int kN = C1 - C0;
+  constexpr int kT0 = C0 / WPK;
+  constexpr int kT1 = ((C1 - 1) / WPK < KH - 1) ? (C1 - 1) / WPK : KH - 1;
+  uint32_t w[kN];
+#pragma unroll
+  for (int i = 0; i < kN; ++i) w[i] = 0u;
+#pragma unroll
+  for (int t = kT0; t <= kT1; ++t) {
+    const uint32_t a = src + (((e0 + static_cast<uint32_t>(t) * tap_step) >> 1) << 2);
+    uint32_t v[WPK + 1];
+#pragma unroll
+    for (int j = 0; j <= WPK; ++j)
+      if (ODD || j < WPK) v[j] = lds_u32(a + 4 * j);
+#pragma unroll
+    for (int j = 0; j < WPK; ++j) {
+      const int k = t * WPK + j;
+      if (k >= C0 && k < C1) {
+        uint32_t x = ODD ? __funnelshift_r(v[j], v[j + 1], 16) : v[j];
+        if (j == WPK - 1) x &= last_mask;
+        w[k - C0] = x;
+      }
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kN; c += 8) tmem_st_n<8>(abase + C0 + c, w + c);
+}
+
+template <int BN, int KH, int WPK>
+__global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __grid_constant__ RowpackParams p) {
+  using Cfg = RowpackCfg<BN>;
+  constexpr int kWords = (KH * WPK + 7) / 8 * 8;   // TMEM columns of one A buffer
+  constexpr int kSteps = kWords / 8;               // K16 steps per plane
+  constexpr int kHalfCols = (kSteps + 1) / 2 * 8;  // builder half 0: columns [0, kHalfCols), half 1: the rest
+  static_assert(kRpSlots * BN <= kRpACol && kRpACol + 2 * kWords <= 512, "TMEM budget");
+
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  const int S = p.stages;
+  const int b_rows = p.kd * p.kp;
+  uint8_t* sB = smem;
+  uint8_t* epi = sB + static_cast<size_t>(b_rows) * Cfg::kBRowBytes;  // 1024-aligned (host)
+  uint8_t* raw = epi + 2 * p.stage_bytes;
+  uint64_t* rfull = reinterpret_cast<uint64_t*>(raw + static_cast<size_t>(S) * p.slot_bytes);
+  uint64_t* rempty = rfull + S;
+  uint64_t* afull = rempty + S;       // [2]
+  uint64_t* afree = afull + 2;        // [2]
+  uint64_t* tfull = afree + 2;        // [kRpSlots]
+  uint64_t* tempty = tfull + kRpSlots;  // [kRpSlots]
+  uint64_t* bfull = tempty + kRpSlots;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+
+  if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  if (threadIdx.x == 32 * 12 + 1) {
+    prefetch_tmap(&p.tmX);
+    prefetch_tmap(&p.tmB);
+    prefetch_tmap(&p.tmY);
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < S; ++i) {
+      mbar_init(&rfull[i], 1);
+      mbar_init(&rempty[i], 8);  // the 8 builder warps
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&afull[i], 8);
+      mbar_init(&afree[i], 1);
+    }
+    for (int i = 0; i < kRpSlots; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 128);  // epilogue threads
+    }
+    mbar_init(bfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 13) {
+    tmem_alloc(tmem_slot, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+  pdl_launch_dependents();
+  // block 0's SM-clock trace (tools/cta_timeline.py): producer [2i], MMA [256 + 2i],
+  // epilogue [512 + 2u], builder warp 4 [640 + 3i]
+  unsigned long long* trace = (blockIdx.x == 0) ? p.trace : nullptr;
+  if (trace && threadIdx.x == 0) trace[1023] = clock64();
+
+  // A unit is one spatial tile (n, tile row, tile col) through the whole depth:
+  // input planes di = lo .. hi in order; plane di feeds output depths
+  // od in [od_first(di), od_last(di)] with kd = di - (od*sd - pd) (depth dilation 1).
+  auto decompose = [&](int u, int& n, int& th, int& tw) {
+    tw = u % p.tiles_w;
+    const int r = u / p.tiles_w;
+    th = r % p.tiles_h;
+    n = r / p.tiles_h;
+  };
+  const int plane_lo = 0 > -p.pd ? 0 : -p.pd;  // first plane any output depth reads
+  int plane_hi = (p.od - 1) * p.sd - p.pd + p.kd - 1;
+  if (plane_hi > p.d - 1) plane_hi = p.d - 1;
+  // (stride 1 / 2 divide by shifts; the general stride keeps the division)
+  auto div_sd = [&](int x) { return p.sd == 1 ? x : p.sd == 2 ? (x >> 1) : x / p.sd; };  // x >= 0
+  auto od_range = [&](int di, int& o0, int& o1) {
+    const int t = di + p.pd - (p.kd - 1);  // od*sd >= t
+    o0 = t <= 0 ? 0 : div_sd(t + p.sd - 1);
+    o1 = div_sd(di + p.pd);
+    if (o1 > p.od - 1) o1 = p.od - 1;
+  };
+
+  if (warp == 12 || warp >= 14) {
+    // ------------------------------------------------------------ producers
+    // One raw box (box_h short rows) per plane; a TMA issue costs an issuing warp
+    // ~1000+ cycles for such a box, so 4 producer warps take planes it = pw (mod 4).
+    const int pw = warp == 12 ? 0 : static_cast<int>(warp) - 13;
+    if (elect_one()) {
+      pdl_wait();  // X / W may be produced by the preceding kernels
+      if (pw == 0) {
+        trace_event(p.trace, TR_PDL_DONE);
+        if (static_cast<int>(blockIdx.x) < p.total_units) {
+          // the packed weight panel, resident for the whole kernel: one box per kd
+          mbar_arrive_expect_tx(bfull, static_cast<uint32_t>(b_rows) * Cfg::kBRowBytes);
+          for (int k = 0; k < p.kd; ++k)
+            tma_load_2d(sB + static_cast<size_t>(k) * p.kp * Cfg::kBRowBytes, &p.tmB, bfull, 0, k * p.kp);
+        }
+      }
+      int it = 0;
+      for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+        int n, th, tw;
+        decompose(u, n, th, tw);
+        // the box starts `shift` elements before the tile's first input element (16-byte aligned)
+        const int x0 = (tw * p.Wt * p.sw - p.pw) * p.ci - p.shift;
+        const int y0 = th * p.R * p.sh - p.ph;
+        for (int di = plane_lo; di <= plane_hi; ++di) {
+          int o0, o1;
+          od_range(di, o0, o1);
+          if (o0 > o1) continue;
+          if ((it & (kRpProducers - 1)) == pw) {
+            const uint32_t slot = static_cast<uint32_t>(it % S), phase = static_cast<uint32_t>(it / S) & 1u;
+            mbar_wait(&rempty[slot], phase ^ 1);
+            if (trace && it < 128) trace[2 * it] = clock64();
+            mbar_arrive_expect_tx(&rfull[slot], static_cast<uint32_t>(p.box_w * p.box_h * 2));
+            tma_load_3d(raw + static_cast<size_t>(slot) * p.slot_bytes, &p.tmX, &rfull[slot], x0, y0,
+                        n * p.d + di);
+            if (trace && it < 128) trace[2 * it + 1] = clock64();
+          }
+          ++it;
+        }
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // ------------------------------------------------------------ builders
+    // warp 4 + 4*half + q: TMEM lane quadrant q, K-vector columns of its half
+    const int bw = static_cast<int>(warp) - 4;
+    const int q = bw & 3, half = bw >> 2;
+    const int m = q * 32 + static_cast<int>(lane);
+    const bool live = m < p.R * p.Wt;
+    const int r = live ? m / p.Wt : 0, c = live ? m % p.Wt : 0;  // dead lanes copy pixel 0
+    // element offset of the lane's first tap run in the raw box (row sh*r, column
+    // shift + sw*CI*c; tap kh adds dh*kh rows); tap_step is even (box_w % 8 == 0)
+    const uint32_t e0 = static_cast<uint32_t>(r * p.sh) * static_cast<uint32_t>(p.box_w) +
+                        static_cast<uint32_t>(p.shift + c * p.sw * p.ci);
+    const uint32_t tap_step = static_cast<uint32_t>(p.dh) * static_cast<uint32_t>(p.box_w);
+    const bool odd = (p.shift & 1) != 0;
+    const uint32_t last_mask = p.mask_last ? 0xFFFFu : 0xFFFFFFFFu;
+    const uint32_t lane_base = tmem_base + ((static_cast<uint32_t>(q) * 32u) << 16) + kRpACol;
+    const uint32_t raw_s = smem_u32(raw);
+    uint32_t slot = 0, phase = 0;
+    uint32_t pi = 0;  // plane counter (A buffer = pi & 1)
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+      for (int di = plane_lo; di <= plane_hi; ++di) {
+        int o0, o1;
+        od_range(di, o0, o1);
+        if (o0 > o1) continue;
+        mbar_wait(&rfull[slot], phase);
+        const bool tr = trace && warp == 4 && lane == 0 && pi < 64;
+        if (tr) trace[640 + 3 * pi] = clock64();
+        const uint32_t src = raw_s + slot * static_cast<uint32_t>(p.slot_bytes);
+        const uint32_t ab = pi & 1, use = pi >> 1;
+        mbar_wait(&afree[ab], (use & 1) ^ 1);  // the MMAs of plane pi - 2 are done with buffer ab
+        tc_fence_after();
+        if (tr) trace[641 + 3 * pi] = clock64();
+        const uint32_t abase = lane_base + ab * kWords;
+        if (half == 0) {
+          if (odd) build_cols<0, kHalfCols, KH, WPK, true>(src, e0, tap_step, last_mask, abase);
+          else build_cols<0, kHalfCols, KH, WPK, false>(src, e0, tap_step, last_mask, abase);
+        } else {
+          if (odd) build_cols<kHalfCols, kWords, KH, WPK, true>(src, e0, tap_step, last_mask, abase);
+          else build_cols<kHalfCols, kWords, KH, WPK, false>(src, e0, tap_step, last_mask, abase);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&rempty[slot]);  // raw rows consumed (values are in TMEM / registers)
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&afull[ab]);
+        if (tr) trace[642 + 3 * pi] = clock64();
+        ++pi;
+        if (++slot == static_cast<uint32_t>(S)) {
+          slot = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 13) {
+    // ------------------------------------------------------------ MMA issuer
+    // Accumulators live in a ring of kRpSlots 64-column slots, one per output depth
+    // in flight (output depth g of the CTA's sequence -> slot g % kRpSlots): a
+    // plane feeds up to ceil(KD/sd) depths, and the slot of a finished depth is
+    // drained by the epilogue while the MMAs carry on with the next planes.
+    const uint64_t b0 = smem_desc(smem_u32(sB), b_rows * Cfg::kBRowBytes, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
+    constexpr uint32_t kBk16 = (16 * Cfg::kBRowBytes) >> 4;  // one K16 step of B (descriptor units)
+    const uint32_t kd_step = (static_cast<uint32_t>(p.kp) * Cfg::kBRowBytes) >> 4;
+    if (static_cast<int>(blockIdx.x) < p.total_units) {
+      mbar_wait(bfull, 0);
+      tc_fence_after();
+    }
+    uint32_t pi = 0;
+    int ubase = 0;  // sequence number of the unit's output depth 0
+    bool first_unit = true;
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ubase += p.od) {
+      for (int di = plane_lo; di <= plane_hi; ++di) {
+        int o0, o1;
+        od_range(di, o0, o1);
+        if (o0 > o1) continue;
+        const uint32_t ab = pi & 1, use = pi >> 1;
+        mbar_wait(&afull[ab], use & 1);
+        tc_fence_after();
+        if (trace && lane == 0 && pi < 128) trace[256 + 2 * pi] = clock64();
+        if (first_unit && lane == 0) {
+          trace_event(p.trace, TR_FIRST_FULL);
+          first_unit = false;
+        }
+        const uint32_t a = tmem_base + kRpACol + ab * kWords;
+        for (int od = o0; od <= o1; ++od) {
+          const int g = ubase + od;
+          const uint32_t sl = static_cast<uint32_t>(g % kRpSlots), sph = static_cast<uint32_t>(g / kRpSlots) & 1u;
+          const int base = od * p.sd - p.pd;  // input plane of kd = 0
+          const int kd = di - base;
+          const bool first = di == (base > 0 ? base : 0);  // depth od's planes are contiguous
+          const bool last = di == (base + p.kd - 1 < p.d - 1 ? base + p.kd - 1 : p.d - 1);
+          if (first) {
+            mbar_wait(&tempty[sl], sph ^ 1);
+            tc_fence_after();
+          }
+          if (elect_one()) {
+            const uint32_t d = tmem_base + kRpAccCol + sl * BN;
+            const uint64_t bk = b0 + static_cast<uint32_t>(kd) * kd_step;
+#pragma unroll
+            for (int st = 0; st < kSteps; ++st)
+              umma_f16_ts(d, a + 8 * st, bk + st * kBk16, Cfg::kIdesc, (first && st == 0) ? 0u : 1u);
+            if (last) umma_commit(&tfull[sl]);
+          }
+          __syncwarp();
+        }
+        if (elect_one()) umma_commit(&afree[ab]);
+        __syncwarp();
+        if (trace && lane == 0 && pi < 128) trace[257 + 2 * pi] = clock64();
+        ++pi;
+      }
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ epilogue (TMA store)
+    // thread = TMEM lane = output pixel m of the tile: for each output depth in
+    // order, tcgen05.ld 32 columns -> the pixel's line of a dense [R][Wt][32]
+    // staging box (swizzled 16-byte chunks) -> one bulk tensor store per 32-column
+    // chunk; double-buffered staging.
+    pdl_wait();  // Y may still be read by the preceding kernel
+    const uint32_t q = warp;
+    const int m = static_cast<int>(q * 32 + lane);
+    const bool mine = m < p.R * p.Wt;
+    const int line_bytes = p.out_f16 ? 64 : 128;
+    uint32_t chunk = 0, ui = 0;
+    int ubase = 0;
+    bool first = true;
+    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ubase += p.od) {
+      int n, th, tw;
+      decompose(u, n, th, tw);
+      for (int od = 0; od < p.od; ++od) {
+        const int g = ubase + od;
+        const uint32_t sl = static_cast<uint32_t>(g % kRpSlots), sph = static_cast<uint32_t>(g / kRpSlots) & 1u;
+        mbar_wait(&tfull[sl], sph);
+        tc_fence_after();
+        if (trace && threadIdx.x == 0 && ui < 64) trace[512 + 2 * ui] = clock64();
+        if (first && threadIdx.x == 0) trace_event(p.trace, TR_FIRST_TFULL);
+        first = false;
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 32, ++chunk) {
+          uint32_t r[32];
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + kRpAccCol + sl * BN + c0, r);
+          tmem_ld_wait();
+          uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
+          named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store
+          if (mine) {
+            uint8_t* dst = buf + m * line_bytes;
+            if (p.out_f16) {
+#pragma unroll
+              for (int cc = 0; cc < 4; ++cc) {
+                uint4 o;
+                __half2 h0 = __floats2half2_rn(__uint_as_float(r[8 * cc]), __uint_as_float(r[8 * cc + 1]));
+                __half2 h1 = __floats2half2_rn(__uint_as_float(r[8 * cc + 2]), __uint_as_float(r[8 * cc + 3]));
+                __half2 h2 = __floats2half2_rn(__uint_as_float(r[8 * cc + 4]), __uint_as_float(r[8 * cc + 5]));
+                __half2 h3 = __floats2half2_rn(__uint_as_float(r[8 * cc + 6]), __uint_as_float(r[8 * cc + 7]));
+                o.x = *reinterpret_cast<uint32_t*>(&h0);
+                o.y = *reinterpret_cast<uint32_t*>(&h1);
+                o.z = *reinterpret_cast<uint32_t*>(&h2);
+                o.w = *reinterpret_cast<uint32_t*>(&h3);
+                *reinterpret_cast<uint4*>(dst + ((cc ^ ((m >> 1) & 3)) << 4)) = o;  // SW64
+              }
+            } else {
+#pragma unroll
+              for (int cc = 0; cc < 8; ++cc)
+                *reinterpret_cast<uint4*>(dst + ((cc ^ (m & 7)) << 4)) =
+                    make_uint4(r[4 * cc], r[4 * cc + 1], r[4 * cc + 2], r[4 * cc + 3]);  // SW128
+            }
+          }
+          fence_proxy_async_smem();
+          named_bar_sync(2, 128);
+          if (threadIdx.x == 0) {
+            const int zo = n * p.od + od;
+            if (p.store_mode == 2)
+              tma_reduce_add_4d(&p.tmY, buf, c0, tw * p.Wt, th * p.R, zo);
+            else
+              tma_store_4d(&p.tmY, buf, c0, tw * p.Wt, th * p.R, zo);
+            tma_store_commit();
+            tma_store_wait_read<1>();
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[sl]);
+        if (trace && threadIdx.x == 0 && ui < 64) trace[513 + 2 * ui] = clock64();
+        ++ui;
+      }
+    }
+    if (threadIdx.x == 0) {
+      tma_store_wait_all<0>();
+      trace_event(p.trace, TR_STORES_DONE);
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 13) tmem_dealloc(tmem_base, 512);
+  if (threadIdx.x == 0) trace_event(p.trace, TR_EXIT);
+}
+
+// Packed weight panel: Bp[kd][kh * 2 * WPK + kw * CI + ci][co] = W[kd][kh][kw][ci][co], zero elsewhere
+// (the layout of the TMEM K vector; Kp = 16 * ksteps rows per kd).
+__global__ void pack_rowpack_weights_kernel(const uint16_t* __restrict__ w, uint16_t* __restrict__ y, int32_t kd,
+                                            int32_t kh, int32_t kw, int32_t ci, int32_t co, int32_t wpk,
+                                            int32_t kp) {
+  const int64_t total = static_cast<int64_t>(kd) * kp * co;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int32_t col = static_cast<int32_t>(i % co);
+    const int64_t row = i / co;
+    const int32_t d = static_cast<int32_t>(row / kp);
+    const int32_t k = static_cast<int32_t>(row - static_cast<int64_t>(d) * kp);
+    const int32_t t = k / (2 * wpk), e = k - t * 2 * wpk;
+    uint16_t v = 0;
+    if (t < kh && e < kw * ci) v = w[((static_cast<int64_t>(d) * kh + t) * kw * ci + e) * co + col];
+    y[i] = v;
+  }
+}
+
+}  // namespace tb

@@ -25,6 +25,7 @@
 #include "netops.cuh"
 #include "options.h"
 #include "prep.cuh"
+#include "rowpack.cuh"
 
 namespace {
 
@@ -960,6 +961,160 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
   return kNotEligible;
 }
 
+// ------------------------------------------------------------------ conv (rowpack, CI = 3 stems)
+
+template <int BN, int KH, int WPK>
+int launch_rowpack(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, WPK>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  const DeviceInfo di = device_info();
+  const int grid = std::min(p.total_units, di.sms);
+  p.trace = g_trace;
+  CUDA_TRY(launch_pdl(tb::conv_rowpack_kernel<BN, KH, WPK>, grid, tb::kRpThreads, smem, stream, p));
+  ++g_launches;
+  return TIR_B200_OK;
+}
+
+// Small-channel convolutions whose (kh, kw, c) window fits one TMEM K vector
+// (rowpack.cuh): the C3D paper shape and the CI = 3 network stems. Returns
+// kNotEligible outside its envelope (the im2col path takes those).
+int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
+                      int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
+  if (tb::options().no_rowpack) return kNotEligible;
+  if (g.transposed || g.g != 1 || epi.on()) return kNotEligible;
+  if (g.co != 64 && g.co != 32) return kNotEligible;
+  if (g.d[2] != 1 || (g.s[2] * g.ci) % 2) return kNotEligible;  // one even-aligned (kw, c) run per tap
+  if (accumulate && Yin != Y) return kNotEligible;               // in-place accumulate = TMA reduce-add
+  const int64_t kwc = g.k[2] * g.ci;
+  const int64_t wpk = (kwc + 1) / 2;
+  const int64_t KH = g.k[1];
+  // instantiated window shapes: 7 taps x 11 words (7x7 CI = 3), 3 taps x 5 words (3x3 CI = 3)
+  if (!((KH == 7 && wpk == 11) || (KH == 3 && wpk == 5))) return kNotEligible;
+  const int64_t kwords = (KH * wpk + 7) / 8 * 8;
+  const int64_t kp = 2 * kwords;
+  const int64_t OD = g.out[0], OH = g.out[1], OW = g.out[2];
+  const int64_t Wt = std::min<int64_t>(16, OW);
+  const int64_t R = 128 / Wt;
+  // TMA box starts are 16-byte aligned in the innermost dim: the box begins `shift`
+  // elements before the tile's first input element (the same shift for every tile
+  // column when Wt*sw*CI % 8 == 0); runs starting at odd elements are funnel-shifted
+  const int64_t tiles_w0 = (OW + Wt - 1) / Wt;
+  if (tiles_w0 > 1 && (Wt * g.s[2] * g.ci) % 8) return kNotEligible;
+  const int64_t shift = (8 - (g.p[2] * g.ci) % 8) % 8;
+  int64_t box_w = (shift + (Wt - 1) * g.s[2] * g.ci + 2 * wpk + 1 + 7) / 8 * 8;
+  // A warp's lanes cover two tile rows (Wt = 16): a row step of 16 (mod 32) words
+  // keeps the builders' 32-bit shared loads conflict-free (lane c reads word 3c + ...)
+  for (int64_t b = box_w; b <= box_w + 56 && b <= 256; b += 8) {
+    if (Wt == 16 && (g.s[1] * b / 2) % 32 == 16) {
+      box_w = b;
+      break;
+    }
+  }
+  const int64_t box_h = (R - 1) * g.s[1] + (KH - 1) * g.d[1] + 1;
+  if (box_w > 256 || box_h > 256) return kNotEligible;
+  const int64_t wci = g.in[2] * g.ci;
+  if ((wci * 2) % 16) return kNotEligible;  // TMA row pitch
+  if (g.d[0] != 1 || (g.k[0] + g.s[0] - 1) / g.s[0] > tb::kRpSlots - 1) return kNotEligible;  // depth window
+  const DeviceInfo di = device_info();
+  const int bn = static_cast<int>(g.co);
+  const int64_t b_bytes = g.k[0] * kp * bn * 2;
+  const int stage_bytes = static_cast<int>((R * Wt * 32 * (out_f16 ? 2 : 4) + 1023) / 1024 * 1024);
+  const int slot_bytes = static_cast<int>((box_w * box_h * 2 + 1023) / 1024 * 1024);
+  const int64_t fixed = 1024 + b_bytes + 2 * stage_bytes + 256;
+  // deep raw ring: each plane's box is a latency-bound handful of short DRAM rows
+  const int stages = static_cast<int>(std::min<int64_t>(8, (di.smem_optin - fixed) / slot_bytes));
+  if (stages < 2) return kNotEligible;
+  const size_t smem = static_cast<size_t>(fixed + static_cast<int64_t>(stages) * slot_bytes);
+  const int64_t tiles_h = (OH + R - 1) / R, tiles_w = (OW + Wt - 1) / Wt;
+  const int64_t units = g.n * tiles_h * tiles_w;  // a unit: one spatial tile through the whole depth
+  if (units >= (1ll << 31) || g.n * g.in[0] >= (1ll << 31)) return kNotEligible;
+
+  // packed weight panel [KD * Kp, CO] in the per-stream workspace
+  void* ws = nullptr;
+  int rc = workspace(static_cast<size_t>(b_bytes) + 256, stream, &ws);
+  if (rc) return rc;
+  uint16_t* Bp = static_cast<uint16_t*>(ws);
+  tb::pack_rowpack_weights_kernel<<<tb::grid_for(g.k[0] * kp * bn), 256, 0, stream>>>(
+      W, Bp, static_cast<int32_t>(g.k[0]), static_cast<int32_t>(KH), static_cast<int32_t>(g.k[2]),
+      static_cast<int32_t>(g.ci), bn, static_cast<int32_t>(wpk), static_cast<int32_t>(kp));
+  CUDA_TRY(cudaGetLastError());
+  ++g_launches;
+
+  tb::RowpackParams p;
+  std::memset(&p, 0, sizeof p);
+  const Driver* drv = driver();
+  if (!drv->tiled) return set_err(TIR_B200_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+  {  // X as 3-D [N*D, H, W*CI]: box {box_w, box_h, 1}; OOB -> zero padding
+    cuuint64_t dims[3] = {static_cast<cuuint64_t>(wci), static_cast<cuuint64_t>(g.in[1]),
+                          static_cast<cuuint64_t>(g.n * g.in[0])};
+    cuuint64_t strides[2] = {static_cast<cuuint64_t>(wci * 2), static_cast<cuuint64_t>(wci * 2 * g.in[1])};
+    cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = drv->tiled(&p.tmX, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<uint16_t*>(X), dims, strides,
+                            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "rowpack X tensor map failed (%d)", (int)r);
+  }
+  {  // packed weights [KD*Kp, CO]: one box of Kp rows per kd
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(bn), static_cast<cuuint64_t>(g.k[0] * kp)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(bn * 2)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(bn), static_cast<cuuint32_t>(kp)};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = drv->tiled(&p.tmB, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, Bp, dims, strides, box, es,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            bn == 64 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "rowpack W tensor map failed (%d)", (int)r);
+  }
+  {  // Y as 4-D [N*OD, OH, OW, CO]: box {32, Wt, R, 1}
+    const int esz = out_f16 ? 2 : 4;
+    cuuint64_t dims[4] = {static_cast<cuuint64_t>(g.co), static_cast<cuuint64_t>(OW), static_cast<cuuint64_t>(OH),
+                          static_cast<cuuint64_t>(g.n * OD)};
+    cuuint64_t strides[3] = {static_cast<cuuint64_t>(g.co * esz), static_cast<cuuint64_t>(g.co * esz * OW),
+                             static_cast<cuuint64_t>(g.co * esz * OW * OH)};
+    cuuint32_t box[4] = {32, static_cast<cuuint32_t>(Wt), static_cast<cuuint32_t>(R), 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = drv->tiled(&p.tmY, out_f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4,
+                            Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            out_f16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                            CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_err(TIR_B200_ERR_CUDA, "rowpack Y tensor map failed (%d)", (int)r);
+  }
+  p.n = static_cast<int32_t>(g.n);
+  p.d = static_cast<int32_t>(g.in[0]);
+  p.ci = static_cast<int32_t>(g.ci);
+  p.od = static_cast<int32_t>(OD);
+  p.oh = static_cast<int32_t>(OH);
+  p.ow = static_cast<int32_t>(OW);
+  p.kd = static_cast<int32_t>(g.k[0]);
+  p.sd = static_cast<int32_t>(g.s[0]);
+  p.sh = static_cast<int32_t>(g.s[1]);
+  p.sw = static_cast<int32_t>(g.s[2]);
+  p.pd = static_cast<int32_t>(g.p[0]);
+  p.ph = static_cast<int32_t>(g.p[1]);
+  p.pw = static_cast<int32_t>(g.p[2]);
+  p.dd = static_cast<int32_t>(g.d[0]);
+  p.dh = static_cast<int32_t>(g.d[1]);
+  p.R = static_cast<int32_t>(R);
+  p.Wt = static_cast<int32_t>(Wt);
+  p.tiles_h = static_cast<int32_t>(tiles_h);
+  p.tiles_w = static_cast<int32_t>(tiles_w);
+  p.total_units = static_cast<int32_t>(units);
+  p.kp = static_cast<int32_t>(kp);
+  p.box_w = static_cast<int32_t>(box_w);
+  p.box_h = static_cast<int32_t>(box_h);
+  p.shift = static_cast<int32_t>(shift);
+  p.stages = stages;
+  p.slot_bytes = slot_bytes;
+  p.mask_last = static_cast<int32_t>(kwc % 2);
+  p.out_f16 = out_f16;
+  p.store_mode = accumulate ? 2 : 1;
+  p.stage_bytes = stage_bytes;
+  if (bn == 64)
+    return KH == 7 ? launch_rowpack<64, 7, 11>(p, smem, stream) : launch_rowpack<64, 3, 5>(p, smem, stream);
+  return KH == 7 ? launch_rowpack<32, 7, 11>(p, smem, stream) : launch_rowpack<32, 3, 5>(p, smem, stream);
+}
+
 int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,
                  int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   Geo g = g0;
@@ -1376,6 +1531,8 @@ int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t*
     if (!is_depthwise(g)) return set_err(TIR_B200_ERR_VALUE, "DEP requires groups == ci == co");
     return dep_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   }
+  rc = conv_rowpack_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+  if (rc != kNotEligible) return rc;
   rc = conv_halo_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
   if (rc != kNotEligible) return rc;
   return conv_tc_impl(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);

@@ -56,6 +56,13 @@ SMALL = {
     "C2D_ci96_co40": tb.Conv("C2D", n=1, in_dhw=(1, 7, 10), ci=96, co=40, k=(1, 3, 5), p=(0, 1, 2)),
     "C3D": tb.Conv("C3D", n=1, in_dhw=(6, 12, 12), ci=3, co=64, k=(7, 7, 7), s=(2, 2, 2), p=(3, 3, 3)),
     "C3D_ci16": tb.Conv("C3D", n=2, in_dhw=(4, 6, 6), ci=16, co=32, k=(3, 3, 3), p=(1, 1, 1)),
+    # rowpack kernel (A operand packed in TMEM, rowpack.cuh): partial tiles in h and w, two depth groups
+    "C3D_rp": tb.Conv("C3D", n=2, in_dhw=(7, 24, 40), ci=3, co=64, k=(7, 7, 7), s=(2, 2, 2), p=(3, 3, 3)),
+    # CO = 32 (SW64 weight panel) and an odd output depth count (a one-depth group)
+    "C3D_rp_odd": tb.Conv("C3D", n=1, in_dhw=(5, 16, 16), ci=3, co=32, k=(7, 7, 7), s=(2, 2, 2), p=(3, 3, 3)),
+    # 2-D stems: ResNet-50's 7x7 s2 and MobileNet-V2's 3x3 s2 (CI = 3)
+    "C2D_stem7": tb.Conv("C2D", n=2, in_dhw=(1, 32, 32), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3)),
+    "C2D_stem3": tb.Conv("C2D", n=2, in_dhw=(1, 24, 40), ci=3, co=32, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1)),
     "DIL": tb.Conv("DIL", n=1, in_dhw=(1, 30, 30), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3), d=(1, 2, 2)),
     "DIL_ci64": tb.Conv("DIL", n=2, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), p=(0, 2, 2), d=(1, 2, 2)),
     "GRP": tb.Conv("GRP", n=2, in_dhw=(1, 12, 12), ci=64, co=128, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), groups=4),
@@ -103,7 +110,7 @@ def test_conv_d2_within_tolerance(name, cuda):
         assert O.tensors_bitwise_equal(got, want)
 
 
-@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D"])
+@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D", "C3D_rp", "C2D_stem3"])
 def test_conv_accumulate_and_fp16_out(name, cuda):
     import torch
 
@@ -323,6 +330,36 @@ def test_planner_switches_exact(switch, option, cuda):
             assert O.tensors_bitwise_equal(got[img:img + 1], want), (switch, img)
             ref16 = np.maximum(want + bias, 0).astype(np.float16).astype(np.float32)
             assert np.array_equal(fused[img:img + 1], ref16), (switch, img)
+
+
+def kernels_launched(fn):
+    """Names of the CUDA kernels `fn` launches (torch profiler / CUPTI)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+
+    with profile(activities=[ProfilerActivity.CUDA]) as prof:
+        fn()
+        torch.cuda.synchronize()
+    return [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+
+
+@pytest.mark.parametrize("name", ["C3D_rp", "C3D_rp_odd", "C2D_stem7", "C2D_stem3"])
+def test_rowpack_vs_im2col_exact(name, option, cuda):
+    """The rowpack kernel (default for these shapes: A operand packed in TMEM) and the
+    (kw, c) relayout + im2col path (no_rowpack = 1) both equal the oracle bit for bit."""
+    spec = SMALL[name]
+    x = O.reference_tensor(spec.x_shape(), 33)
+    w = O.reference_tensor(spec.w_shape(), 34)
+    want = O.conv(ospec(spec), x, w, threads=8)
+    out = {}
+    names = kernels_launched(lambda: out.setdefault("y", run_conv(spec, x, w, cuda)))
+    assert any("conv_rowpack_kernel" in k for k in names), names
+    assert O.tensors_bitwise_equal(out["y"], want)
+    option("no_rowpack", 1)
+    out = {}
+    names = kernels_launched(lambda: out.setdefault("y", run_conv(spec, x, w, cuda)))
+    assert not any("conv_rowpack_kernel" in k for k in names), names
+    assert O.tensors_bitwise_equal(out["y"], want)
 
 
 @pytest.mark.parametrize("name", ["DIL", "C3D"])

@@ -95,6 +95,9 @@ def main():
         print("  producer (empty ok, issued):", prod[:12])
         print("  mma (round start, round end):", mma[:12])
         print("  epilogue (tfull ok, done):", epi[:12])
+        bld = [tuple(clk[640 + 3 * i + j] - t0 for j in range(3)) for i in range(64) if clk[640 + 3 * i]]
+        if bld:
+            print("  builder warp (raw ok, A buffer free, A published):", bld[:16])
     print(f"launch {k-1} exits: first {pe[0]} p10 {pe[len(pe)//10]} median {pe[len(pe)//2]} p90 {pe[9*len(pe)//10]} last {pe[-1]}")
 
 

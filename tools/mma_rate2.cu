@@ -12,6 +12,8 @@
 
 using namespace tb;
 
+__device__ __forceinline__ void umma_ts_(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t acc);
 __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                         uint32_t acc) {
   asm volatile(
@@ -19,6 +21,11 @@ __device__ __forceinline__ void umma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
+}
+
+__device__ __forceinline__ void umma_ts_(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                         uint32_t acc) {
+  umma_ts(tmem_d, tmem_a, bdesc, idesc, acc);
 }
 
 // mode 0: SS B MN-major, 1: SS B K-major, 2: TS B MN-major, 3: TS B K-major
@@ -99,6 +106,77 @@ __global__ void tmem_st_kernel(int iters, unsigned long long* out) {
   if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
 }
 
+
+// rowpack-like TS MMA stream: per "plane" 4 accumulators x 10 K16 steps, B walks a
+// 140 KB panel (7 kd chunks); warps 4..11 optionally load shared memory (lds=1) or
+// store 80 TMEM columns (st=1) per plane like the builders.
+__global__ void rp_like(int planes, int lds, int st, unsigned long long* out) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tslot;
+  __shared__ volatile int stop;
+  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x) ((uint4*)smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); stop = 0; }
+  if (threadIdx.x < 32) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
+  asm volatile("fence.proxy.async.shared::cta;");
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tslot;
+  const int warp = threadIdx.x / 32;
+  if (warp == 0) {
+    const uint64_t b0 = smem_desc(smem_u32(smem), 143360, 1024, 2);
+    const uint32_t idesc = idesc_f16_f32(128, 64, 0, 1);
+    unsigned long long t0 = clock64();
+    if (elect_one()) {
+      for (int pl = 0; pl < planes; ++pl) {
+        const uint32_t a = tmem + 320 + 80 * (pl & 1);
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t d = tmem + 64 * ((pl + j) % 5);
+          const uint64_t bk = b0 + ((pl + j) % 7) * ((160 * 128) >> 4);
+#pragma unroll
+          for (int s = 0; s < 10; ++s) umma_ts_(d, a + 8 * s, bk + s * 128, idesc, 1);
+        }
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+    mbar_wait(&bar, 0);
+    unsigned long long t1 = clock64();
+    if (threadIdx.x == 0) { out[blockIdx.x] = (t1 - t0) / planes; stop = 1; }
+  } else if (warp >= 4 && warp < 12) {
+    const uint32_t base = smem_u32(smem) + 143360 + (threadIdx.x & 31) * 12;
+    uint32_t acc = 0;
+    const uint32_t q = warp & 3;
+    while (!stop) {
+      if (lds) {
+#pragma unroll 4
+        for (int i = 0; i < 48; ++i) {
+          uint32_t v;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(base + 4 * (i % 12) + 240 * (i / 12)));
+          acc += v;
+        }
+      }
+      if (st) {
+        uint32_t w[8];
+        for (int i = 0; i < 8; ++i) w[i] = acc + i;
+        for (int c = 0; c < 40; c += 8) {
+          const uint32_t ta = tmem + ((q * 32u) << 16) + 320 + 80 * (acc & 1) + (warp >= 8 ? 40 : 0) + c;
+          asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+                       "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7]));
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;");
+      }
+      __nanosleep(100);
+    }
+    if (acc == 12345) out[1000] = acc;
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tmem_dealloc(tmem, 512);
+}
+
 template <int N, int mode>
 void run(int grid, int step) {
   unsigned long long* d;
@@ -125,6 +203,22 @@ int main() {
   run<64, 2>(148, 1); run<128, 2>(148, 1); run<256, 2>(148, 0);
   run<64, 3>(148, 1); run<128, 3>(148, 1); run<256, 3>(148, 0);
   run<32, 2>(148, 0);
+  {
+    unsigned long long* d;
+    cudaMalloc(&d, 2000 * 8);
+    cudaFuncSetAttribute(rp_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    for (int cfg = 0; cfg < 4; ++cfg) {
+      const int lds = cfg & 1, st = cfg >> 1;
+      rp_like<<<148, 384, 200 * 1024>>>(256, lds, st, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      unsigned long long h[148];
+      cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += h[i];
+      printf("rowpack-like plane (40 TS MMAs, 4 accumulators, B over 7 chunks) lds=%d st=%d: %.0f cycles/plane (ideal 1280) %s\n",
+             lds, st, avg / 148, e ? cudaGetErrorString(e) : "");
+    }
+  }
   {
     unsigned long long* d;
     cudaMalloc(&d, 148 * 8);
