@@ -53,6 +53,7 @@ struct alignas(64) RowpackParams {
   int32_t mask_last;  // KW*CI odd: the last word of each tap keeps only its low half
   int32_t out_f16, store_mode;  // store_mode 1: TMA store, 2: TMA reduce-add (Y += conv)
   int32_t stage_bytes;
+  int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output stores
   unsigned long long* trace;
 };
 
@@ -345,7 +346,13 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         tc_fence_after();
         if (tr) trace[641 + 3 * pi] = clock64();
         const uint32_t abase = lane_base + ab * kWords;
-        if (half == 0) {
+        if (p.debug & 1) {
+          uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+          if (half == 0)
+            for (int c0 = 0; c0 < kHalfCols; c0 += 8) tmem_st_n<8>(abase + c0, z);
+          else
+            for (int c0 = kHalfCols; c0 < kWords; c0 += 8) tmem_st_n<8>(abase + c0, z);
+        } else if (half == 0) {
           if (odd) build_cols<0, kHalfCols, KH, WPK, true>(src, e0, tap_step, last_mask, abase);
           else build_cols<0, kHalfCols, KH, WPK, false>(src, e0, tap_step, last_mask, abase);
         } else {
@@ -416,6 +423,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
             if (last) umma_commit(&tfull[sl]);
           }
           __syncwarp();
+          if (trace && lane == 0 && pi < 48 && od - o0 < 4) trace[832 + 4 * pi + (od - o0)] = clock64();
         }
         if (elect_one()) umma_commit(&afree[ab]);
         __syncwarp();
@@ -480,7 +488,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           }
           fence_proxy_async_smem();
           named_bar_sync(2, 128);
-          if (threadIdx.x == 0) {
+          if (threadIdx.x == 0 && !(p.debug & 2)) {
             const int zo = n * p.od + od;
             if (p.store_mode == 2)
               tma_reduce_add_4d(&p.tmY, buf, c0, tw * p.Wt, th * p.R, zo);

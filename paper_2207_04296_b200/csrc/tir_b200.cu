@@ -1110,6 +1110,7 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   p.out_f16 = out_f16;
   p.store_mode = accumulate ? 2 : 1;
   p.stage_bytes = stage_bytes;
+  p.debug = tb::options().rowpack_debug;
   if (bn == 64)
     return KH == 7 ? launch_rowpack<64, 7, 11>(p, smem, stream) : launch_rowpack<64, 3, 5>(p, smem, stream);
   return KH == 7 ? launch_rowpack<32, 7, 11>(p, smem, stream) : launch_rowpack<32, 3, 5>(p, smem, stream);

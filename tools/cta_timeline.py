@@ -98,6 +98,10 @@ def main():
         bld = [tuple(clk[640 + 3 * i + j] - t0 for j in range(3)) for i in range(64) if clk[640 + 3 * i]]
         if bld:
             print("  builder warp (raw ok, A buffer free, A published):", bld[:16])
+        ods = [[clk[832 + 4 * i + j] - t0 for j in range(4) if clk[832 + 4 * i + j]] for i in range(48)
+               if clk[832 + 4 * i]]
+        if ods:
+            print("  MMA per-depth issue done (rowpack):", ods[:16])
     print(f"launch {k-1} exits: first {pe[0]} p10 {pe[len(pe)//10]} median {pe[len(pe)//2]} p90 {pe[9*len(pe)//10]} last {pe[-1]}")
 
 

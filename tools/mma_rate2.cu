@@ -107,17 +107,33 @@ __global__ void tmem_st_kernel(int iters, unsigned long long* out) {
 }
 
 
+__device__ __forceinline__ void tmem_st_n32_(uint32_t t, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+      "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(t),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
+      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]),
+      "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]),
+      "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31]));
+}
+
 // rowpack-like TS MMA stream: per "plane" 4 accumulators x 10 K16 steps, B walks a
 // 140 KB panel (7 kd chunks); warps 4..11 optionally load shared memory (lds=1) or
 // store 80 TMEM columns (st=1) per plane like the builders.
-__global__ void rp_like(int planes, int lds, int st, unsigned long long* out) {
+__global__ void rp_like(int planes, int lds, int st, int ld, unsigned long long* out, int fence = 0, int rnd = 0) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   __shared__ __align__(8) uint64_t bar;
   __shared__ uint32_t tslot;
   __shared__ volatile int stop;
-  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x) ((uint4*)smem)[i] = make_uint4(0, 0, 0, 0);
-  if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); stop = 0; }
+  __shared__ __align__(8) uint64_t bar2;
+  for (int i = threadIdx.x; i < 160 * 1024 / 16; i += blockDim.x) {
+    uint32_t h = rnd ? (i * 2654435761u) ^ (i >> 3) : 0u;
+    // random fp16 pairs in [-2, 2) (exponent bits bounded), or zeros
+    uint32_t v = rnd ? ((h & 0x83FF83FFu) | 0x3C003C00u) : 0u;
+    ((uint4*)smem)[i] = make_uint4(v, v ^ 0x00050003u, v ^ 0x01100220u, v ^ 0x80008000u);
+  }
+  if (threadIdx.x == 0) { mbar_init(&bar, 1); mbar_init(&bar2, 1); fence_barrier_init(); stop = 0; }
   if (threadIdx.x < 32) { tmem_alloc(&tslot, 512); tmem_relinquish(); }
   asm volatile("fence.proxy.async.shared::cta;");
   tc_fence_before();
@@ -125,6 +141,18 @@ __global__ void rp_like(int planes, int lds, int st, unsigned long long* out) {
   tc_fence_after();
   const uint32_t tmem = tslot;
   const int warp = threadIdx.x / 32;
+  if (rnd && warp < 4) {  // random A buffers in TMEM
+    uint32_t w[32];
+    for (int i = 0; i < 32; ++i) {
+      uint32_t h = (threadIdx.x * 97u + i * 2654435761u);
+      w[i] = (h & 0x83FF83FFu) | 0x3C003C00u;
+    }
+    for (int c = 0; c < 160; c += 32) tmem_st_n32_(tmem + ((warp * 32u) << 16) + 320 + c, w);
+    asm volatile("tcgen05.wait::st.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
   if (warp == 0) {
     const uint64_t b0 = smem_desc(smem_u32(smem), 143360, 1024, 2);
     const uint32_t idesc = idesc_f16_f32(128, 64, 0, 1);
@@ -132,7 +160,10 @@ __global__ void rp_like(int planes, int lds, int st, unsigned long long* out) {
     if (elect_one()) {
       for (int pl = 0; pl < planes; ++pl) {
         const uint32_t a = tmem + 320 + 80 * (pl & 1);
+        if (fence & 1) tc_fence_after();
+        if (fence & 4) umma_commit(&bar2);
         for (int j = 0; j < 4; ++j) {
+          if (fence & 2) tc_fence_after();
           const uint32_t d = tmem + 64 * ((pl + j) % 5);
           const uint64_t bk = b0 + ((pl + j) % 7) * ((160 * 128) >> 4);
 #pragma unroll
@@ -168,9 +199,22 @@ __global__ void rp_like(int planes, int lds, int st, unsigned long long* out) {
         }
         asm volatile("tcgen05.wait::st.sync.aligned;");
       }
-      __nanosleep(100);
+      if (lds < 2) __nanosleep(100);
     }
     if (acc == 12345) out[1000] = acc;
+  } else if (warp < 4 && ld) {
+    // epilogue-like: read 64 accumulator columns of the lane quadrant, ~one od per 500 cycles
+    uint32_t acc = 0;
+    while (!stop) {
+      for (int c0 = 0; c0 < 64; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld_32x32b_x32(tmem + ((warp * 32u) << 16) + 64 * (acc % 5) + c0, r);
+        tmem_ld_wait();
+        for (int i = 0; i < 32; ++i) acc += r[i];
+      }
+      __nanosleep(200);
+    }
+    if (acc == 12345) out[1001] = acc;
   }
   tc_fence_before();
   __syncthreads();
@@ -207,16 +251,38 @@ int main() {
     unsigned long long* d;
     cudaMalloc(&d, 2000 * 8);
     cudaFuncSetAttribute(rp_like, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    for (int cfg = 0; cfg < 4; ++cfg) {
-      const int lds = cfg & 1, st = cfg >> 1;
-      rp_like<<<148, 384, 200 * 1024>>>(256, lds, st, d);
+    for (int rnd = 0; rnd < 2; ++rnd) {
+      for (int pl : {256, 20000}) {
+        rp_like<<<148, 384, 200 * 1024>>>(pl, 0, 0, 0, d, 0, rnd);
+        cudaError_t e = cudaDeviceSynchronize();
+        unsigned long long h[148];
+        cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+        double avg = 0;
+        for (int i = 0; i < 148; ++i) avg += h[i];
+        printf("rowpack-like plane, %s operands, %d planes: %.0f cycles/plane %s\n", rnd ? "random" : "zero", pl,
+               avg / 148, e ? cudaGetErrorString(e) : "");
+      }
+    }
+    for (int fence = 1; fence < 2; ++fence) {
+      rp_like<<<148, 384, 200 * 1024>>>(256, 0, 0, 0, d, fence);
       cudaError_t e = cudaDeviceSynchronize();
       unsigned long long h[148];
       cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
       double avg = 0;
       for (int i = 0; i < 148; ++i) avg += h[i];
-      printf("rowpack-like plane (40 TS MMAs, 4 accumulators, B over 7 chunks) lds=%d st=%d: %.0f cycles/plane (ideal 1280) %s\n",
-             lds, st, avg / 148, e ? cudaGetErrorString(e) : "");
+      printf("rowpack-like plane, fence::after per plane %d per depth %d, commit per plane %d: %.0f cycles/plane %s\n",
+             fence & 1, (fence >> 1) & 1, fence >> 2, avg / 148, e ? cudaGetErrorString(e) : "");
+    }
+    for (int cfg = 0; cfg < 8; ++cfg) {
+      const int lds = cfg == 6 ? 2 : cfg == 7 ? 2 : cfg & 1, st = cfg == 7 ? 1 : (cfg >> 1) & 1, ld = cfg == 7 ? 1 : (cfg >> 2) & 1;
+      rp_like<<<148, 384, 200 * 1024>>>(cfg == 7 ? 60000 : 256, lds, st, ld, d);
+      cudaError_t e = cudaDeviceSynchronize();
+      unsigned long long h[148];
+      cudaMemcpy(h, d, 148 * 8, cudaMemcpyDeviceToHost);
+      double avg = 0;
+      for (int i = 0; i < 148; ++i) avg += h[i];
+      printf("rowpack-like plane (40 TS MMAs, 4 accumulators, B over 7 chunks) lds=%d st=%d ld=%d: %.0f cycles/plane (ideal 1280) %s\n",
+             lds, st, ld, avg / 148, e ? cudaGetErrorString(e) : "");
     }
   }
   {
