@@ -160,20 +160,23 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
             if (p.l2_prefetch == 1 || box == static_cast<int>(blockIdx.x) / (p.groups * p.tiles_n))
               tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
       }
-      pdl_wait();  // X / W may be produced by the preceding kernel
-      trace_event(p.trace, TR_PDL_DONE);
+      // the first tile's decomposition and the loop constants before the wait
       const uint32_t slab_tx = static_cast<uint32_t>(p.HR) * p.Wv * 128;
       uint32_t slot = 0, phase = 0;
       int it = 0;
       bool weights_pending = static_cast<int>(blockIdx.x) < p.total_tiles;
+      int n, th, tw, g, nt;
+      decompose(blockIdx.x, n, th, tw, g, nt);
+      pdl_wait();  // X / W may be produced by the preceding kernel
+      trace_event(p.trace, TR_PDL_DONE);
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-        int n, th, tw, g, nt;
-        decompose(tile, n, th, tw, g, nt);
+        if (tile != static_cast<int>(blockIdx.x)) decompose(tile, n, th, tw, g, nt);
         const int y0 = th * p.R - p.pad_h;
         const int x0 = tw * p.Wt - p.pad_w;
         for (int cb = 0; cb < p.cblocks; ++cb, ++it) {
           mbar_wait(&empty[slot], phase ^ 1);
           if (trace && it < 128) trace[2 * it] = clock64();
+          if (it == 0) trace_event(p.trace, TR_FIRST_ISSUE);
           mbar_arrive_expect_tx(&full[slot], slab_tx);
           tma_load_4d(sA0 + slot * slab_bytes, &p.tmX, &full[slot], g * p.cig + cb * 64, x0, y0, n);
           if (trace && it < 128) trace[2 * it + 1] = clock64();

@@ -317,7 +317,8 @@ __device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float
   if (active) {
     pdl_wait();  // Yin / residual may come from the preceding kernel
     constexpr int kV = BN / 4;  // float4 per partial row
-    constexpr int kU = 8;       // items in flight per thread (one remote load each per split)
+    constexpr int kU = 2;       // items per thread and pass
+    constexpr int kMaxK = 8;    // every split's remote load of a pass is in flight at once
     const uint32_t base = smem_u32(part);
     const int valid = p.cog - nt * BN;
     const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
@@ -325,27 +326,31 @@ __device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float
     const int items = (r1 - r0) * kV;
 #pragma unroll 1
     for (int i0 = threadIdx.x; i0 < items; i0 += kU * blockDim.x) {
-      float4 v[kU];
-#pragma unroll 1
-      for (int k = 0; k < ks; ++k) {
-        uint32_t rb;
-        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(base), "r"(k));
-        float4 t[kU];
+      float4 t[kMaxK][kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          const int i = i0 + u * blockDim.x;
-          if (i < items) {
-            const int row = r0 + i / kV, col = (i % kV) * 4;
-            t[u] = ld_cluster_f4(rb + static_cast<uint32_t>((row * (BN + 4) + col) * 4));
+      for (int k = 0; k < kMaxK; ++k) {
+        if (k < ks) {
+          uint32_t rb;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(base), "r"(k));
+#pragma unroll
+          for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * blockDim.x;
+            if (i < items) {
+              const int row = r0 + i / kV, col = (i % kV) * 4;
+              t[k][u] = ld_cluster_f4(rb + static_cast<uint32_t>((row * (BN + 4) + col) * 4));
+            }
           }
         }
+      }
+      float4 v[kU];
 #pragma unroll
-        for (int u = 0; u < kU; ++u) {
-          if (k == 0) {
-            v[u] = t[u];
-          } else {
-            v[u].x = v[u].x + t[u].x; v[u].y = v[u].y + t[u].y;
-            v[u].z = v[u].z + t[u].z; v[u].w = v[u].w + t[u].w;
+      for (int u = 0; u < kU; ++u) {
+        v[u] = t[0][u];
+#pragma unroll
+        for (int k = 1; k < kMaxK; ++k) {  // fixed order ((p_0 + p_1) + p_2) + ...
+          if (k < ks) {
+            v[u].x = v[u].x + t[k][u].x; v[u].y = v[u].y + t[k][u].y;
+            v[u].z = v[u].z + t[k][u].z; v[u].w = v[u].w + t[k][u].w;
           }
         }
       }
@@ -506,8 +511,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
 
   if (warp >= kEpi && warp < kEpi + kProducers) {
     // ------------------------------------------------------------ producers
-    pdl_wait();  // operands may be produced by the preceding kernel
-    if (warp == kEpi && lane == 0) trace_event(p.trace, TR_PDL_DONE);
     // Every producer walks every stage and issues a round-robin share of its
     // TMA requests (pieces j = pw mod 4; B chunks after them), arriving on the
     // stage's full barrier with its own expect_tx. A single issuing thread
@@ -533,6 +536,50 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     if (b_mode == B_STREAM && p.b_kmajor)
       for (int u = 0; u < KS; ++u)
         if ((pps + u) % kProducers == pw) my_tx += BN * 128;
+    // Per-tile producer setup (tile decomposition, im2col base coordinates,
+    // split range): divisions and parameter loads that took ~0.9 us after the
+    // PDL wait for the first tile (tools/cta_timeline.py). The first tile's is
+    // computed before the wait, every next one right after the current tile's
+    // last stage is issued.
+    struct ProdTile {
+      const CUtensorMap* tmA;
+      const int4* ptab;
+      int a_r, a_c, b_r, b_c, m0, n, cx, cy, cz, col0, npieces, cbase, st0, st1;
+    };
+    auto prod_setup = [&](int tile) {
+      ProdTile t;
+      int s, mt, g, nt, ks, z1, z2, lt = mc_tile<CG2>(p, tile);
+      split_batch(p, lt, z1, z2);
+      decompose_tile(p, lt, s, mt, g, nt, ks);
+      t.a_r = batch_row(p.ba, z1, z2);
+      t.a_c = batch_col(p.ba, z1, z2);
+      t.b_r = batch_row(p.bb, z1, z2);
+      t.b_c = batch_col(p.bb, z1, z2);
+      const SubProb& sp = p.sub[s];
+      t.tmA = &p.tmA[s];
+      t.m0 = mt * kBM;
+      const int x = t.m0 % sp.gx;
+      int rest = t.m0 / sp.gx;
+      const int y = rest % sp.gy;
+      rest /= sp.gy;
+      const int z = rest % sp.gz;
+      t.n = rest / sp.gz;
+      t.cx = sp.a_lo[0] + x * sp.a_st[0];
+      t.cy = sp.a_lo[1] + y * sp.a_st[1];
+      t.cz = sp.a_lo[2] + z * sp.a_st[2];
+      t.col0 = g * p.cog + nt * BN;
+      t.npieces = sp.num_pieces;
+      t.cbase = g * p.cig;
+      t.ptab = pieces + sp.piece_begin;
+      split_range(p, sp.num_stages, ks, t.st0, t.st1);
+      return t;
+    };
+    ProdTile pt{};
+    if (static_cast<int>(blockIdx.x) < p.total_tiles) pt = prod_setup(blockIdx.x);
+    // Everything above is parameter arithmetic: it runs before the wait, so
+    // the first TMA issues right after the preceding grid's memory is visible.
+    pdl_wait();  // operands may be produced by the preceding kernel
+    if (warp == kEpi && lane == 0) trace_event(p.trace, TR_PDL_DONE);
     if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
       // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once.
       int s0, mt0, g0, nt0;
@@ -554,32 +601,18 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     uint32_t slot = 0, phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
-      int s, mt, g, nt, ks, z1, z2, lt = mc_tile<CG2>(p, tile);
-      split_batch(p, lt, z1, z2);
-      decompose_tile(p, lt, s, mt, g, nt, ks);
-      const int a_r = batch_row(p.ba, z1, z2), a_c = batch_col(p.ba, z1, z2);
-      const int b_r = batch_row(p.bb, z1, z2), b_c = batch_col(p.bb, z1, z2);
-      const SubProb& sp = p.sub[s];
-      const CUtensorMap* tmA = &p.tmA[s];
-      const int m0 = mt * kBM;
-      int x = m0 % sp.gx, rest = m0 / sp.gx;
-      int y = rest % sp.gy;
-      rest /= sp.gy;
-      int z = rest % sp.gz;
-      const int n = rest / sp.gz;
-      const int cx = sp.a_lo[0] + x * sp.a_st[0];
-      const int cy = sp.a_lo[1] + y * sp.a_st[1];
-      const int cz = sp.a_lo[2] + z * sp.a_st[2];
-      const int col0 = g * p.cog + nt * BN;
-      const int npieces = sp.num_pieces, nst = sp.num_stages;
-      const int cbase = g * p.cig;
-      const int4* ptab = pieces + sp.piece_begin;
-      int st0, st1;
-      split_range(p, nst, ks, st0, st1);
+      const int a_r = pt.a_r, a_c = pt.a_c, b_r = pt.b_r, b_c = pt.b_c;
+      const CUtensorMap* tmA = pt.tmA;
+      const int m0 = pt.m0, n = pt.n, cx = pt.cx, cy = pt.cy, cz = pt.cz;
+      const int col0 = pt.col0, npieces = pt.npieces, cbase = pt.cbase;
+      const int4* ptab = pt.ptab;
+      const int st0 = pt.st0, st1 = pt.st1;
       for (int st = st0; st < st1; ++st, ++it) {
+        if (it == 0 && pw == 0 && lane == 0) trace_event(p.trace, TR_PRELOOP);
         mbar_wait(&empty[slot], phase ^ 1);
         if (elect_one()) {
           if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();
+          if (it == 0 && pw == 0) trace_event(p.trace, TR_FIRST_ISSUE);
           uint8_t* sA = sA0 + slot * Cfg::kABytes;
           uint8_t* sB = sB0 + slot * kBSlotBytes;
           if constexpr (cg2) {
@@ -647,6 +680,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
           phase ^= 1;
         }
       }
+      if (tile + static_cast<int>(gridDim.x) < p.total_tiles) pt = prod_setup(tile + gridDim.x);
     }
   } else if (warp == kMmaWarp) {
     // ------------------------------------------------------------ MMA issuer

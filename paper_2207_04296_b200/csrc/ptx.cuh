@@ -46,7 +46,7 @@ __device__ __forceinline__ bool elect_one() {
 // trace[8192 + 8 * b + event] — only when a trace buffer is set
 // (tir_b200_debug_set_trace; tools/floor_timeline.py). Null in production.
 enum TraceEvent { TR_ENTRY = 0, TR_PDL_DONE = 1, TR_FIRST_FULL = 2, TR_FIRST_TFULL = 3, TR_STORES_DONE = 4,
-                  TR_EXIT = 5 };
+                  TR_EXIT = 5, TR_FIRST_ISSUE = 6, TR_PRELOOP = 7 };
 __device__ __forceinline__ void trace_event(unsigned long long* trace, int ev) {
   if (trace && blockIdx.x < 256) {
     unsigned long long t;

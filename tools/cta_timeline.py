@@ -45,7 +45,7 @@ def capture(op, launches=8):
     torch.cuda.synchronize()
     out = []
     for b in bufs:
-        ev = b[8192:8192 + 8 * 256].view(256, 8)[:, :6].cpu().tolist()
+        ev = b[8192:8192 + 8 * 256].view(256, 8)[:, :8].cpu().tolist()
         cta = b[2048:2048 + 4 * 1024].view(1024, 4).cpu().tolist()
         out.append((ev, cta, b[:1024].cpu().tolist()))
     return out
@@ -66,7 +66,7 @@ def main():
         smid = cta[b][2] if b < len(cta) else -1
         rows.append((tiles, [x - prev_exit if x else None for x in e], smid, b))
     print(f"op {op} launch {k}: {len(rows)} traced CTAs; times in ns relative to launch {k-1}'s last exit")
-    names = ["entry", "pdl", "full", "tfull", "stores", "exit"]
+    names = ["entry", "pdl", "full", "tfull", "stores", "exit", "issue", "preloop"]
     by = {}
     for t, e, s, b in rows:
         by.setdefault(t, []).append(e)
