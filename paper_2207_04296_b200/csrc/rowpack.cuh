@@ -11,9 +11,10 @@
 //     elements of the [W*CI] row (4.7 KB for C3D) — zero fill is the padding;
 //   * 8 builder warps turn it into the packed A operand directly in TMEM: TMEM
 //     lane m = output pixel (m / Wt, m % Wt); its K vector is the kh taps of the
-//     plane back to back, each tap the KW*CI contiguous elements of input row
-//     sh*r + dh*kh starting at element sw*CI*c (one even-aligned run: 32-bit
-//     shared loads, no shuffles), padded to an even count (WPK 32-bit words);
+//     plane back to back, each tap the KW*CI elements of input row sh*r + dh*kh
+//     from element sw*CI*c on (KW runs of CI contiguous elements, dw*CI apart:
+//     32-bit shared loads and one byte permute per word), padded to an even
+//     count (WPK 32-bit words);
 //     tcgen05.st writes them (measured 605 B/clk);
 //   * the MMA warp issues kind::f16 MMAs with A in TMEM (TS mode, 32 cycles per
 //     128x64x16 — the full tensor rate) and B = the packed weight panel, resident
@@ -34,9 +35,8 @@ namespace tb {
 
 constexpr int kRpProducers = 4;   // TMA producer warps (raw boxes of planes it = pw mod 4)
 constexpr int kRpThreads = 544;  // warps 0-3 epilogue, 4-11 builders, 12 + 14-16 producers, 13 MMA
-constexpr int kRpSlots = 5;      // TMEM accumulator ring: output depths in flight (+ one draining)
-constexpr int kRpAccCol = 0;     // TMEM: kRpSlots x BN accumulator columns
-constexpr int kRpACol = 320;     // TMEM: 2 A buffers x KWORDS columns (after the 5 x 64 accumulators)
+constexpr int kRpMaxSlots = 5;   // TMEM accumulator ring (p.nacc slots): output depths in flight + one draining
+constexpr int kRpMaxA = 4;       // TMEM A-buffer ring (p.nabuf buffers of KWORDS columns after the accumulators)
 
 struct alignas(64) RowpackParams {
   CUtensorMap tmX;  // 3-D over X[N*D, H, W*CI] fp16: box {box_w, box_h, 1}, no swizzle
@@ -50,9 +50,9 @@ struct alignas(64) RowpackParams {
   int32_t box_w, box_h;
   int32_t shift;  // elements between the box's 16-byte-aligned start column and the tile's first input element
   int32_t stages, slot_bytes;
-  int32_t mask_last;  // KW*CI odd: the last word of each tap keeps only its low half
   int32_t out_f16, store_mode;  // store_mode 1: TMA store, 2: TMA reduce-add (Y += conv)
   int32_t stage_bytes;
+  int32_t nacc, nabuf;  // TMEM rings: accumulator slots (<= kRpMaxSlots), A buffers (<= kRpMaxA)
   int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output stores
   unsigned long long* trace;
 };
@@ -153,36 +153,55 @@ __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
   return v;
 }
 
+// One tap's (kw, c) window: KW runs of CI contiguous elements, DW*CI elements
+// apart (dilation DW), packed as KW*CI elements padded to an even count (WPK
+// 32-bit words). Element k of the window sits kOff(k) elements past the run start.
+template <int KW, int CI, int DW>
+struct TapWindow {
+  static constexpr int kKwc = KW * CI;
+  static constexpr int kWpk = (kKwc + 1) / 2;
+  static constexpr int kSpan = (KW - 1) * DW * CI + CI;  // elements from the first to past the last
+  __host__ __device__ static constexpr int off(int k) { return (k / CI) * DW * CI + k % CI; }
+};
+
 // Columns [C0, C1) of one lane's TMEM K vector, stored in 8-column tcgen05.st
-// chunks at 8-aligned columns. Column k is word k % WPK of tap k / WPK: elements
-// e, e+1 of the raw rows, e = e0 + tap*tap_step + 2*(k % WPK), e0 the lane's run
-// start. Every run of a kernel starts at the same parity (ODD: two aligned words
-// funnel-shifted); the tap's last word keeps only its low half when KW*CI is odd;
-// columns past KH*WPK are the K padding (zero). Lanes past the tile's pixels
+// chunks at 8-aligned columns. Column k is word k % WPK of tap k / WPK: the
+// window elements 2j, 2j+1 (j = k % WPK) of raw row e0 + tap*tap_step. Every run
+// of a kernel starts at the same element parity (ODD): the aligned words spanning
+// the window are loaded once per tap and each output word is one byte permute of
+// two of them (compile-time selectors). Columns past KH*WPK are the K padding,
+// an odd KW*CI pads each tap with one zero. Lanes past the tile's pixels
 // (r = c = 0) build a copy of pixel 0: their TMEM rows only feed discarded rows.
-template <int C0, int C1, int KH, int WPK, bool ODD>
-__device__ __forceinline__ void build_cols(uint32_t src, uint32_t e0, uint32_t tap_step, uint32_t last_mask,
-                                           uint32_t abase) {
+template <int C0, int C1, int KH, int KW, int CI, int DW, bool ODD>
+__device__ __forceinline__ void build_cols(uint32_t src, uint32_t e0, uint32_t tap_step, uint32_t abase) {
+  using Win = TapWindow<KW, CI, DW>;
+  constexpr int WPK = Win::kWpk;
   constexpr int kN = C1 - C0;
   constexpr int kT0 = C0 / WPK;
   constexpr int kT1 = ((C1 - 1) / WPK < KH - 1) ? (C1 - 1) / WPK : KH - 1;
+  constexpr int kNW = (Win::kSpan + (ODD ? 1 : 0) + 1) / 2;  // aligned words covering the window
   uint32_t w[kN];
 #pragma unroll
   for (int i = 0; i < kN; ++i) w[i] = 0u;
 #pragma unroll
   for (int t = kT0; t <= kT1; ++t) {
     const uint32_t a = src + (((e0 + static_cast<uint32_t>(t) * tap_step) >> 1) << 2);
-    uint32_t v[WPK + 1];
+    uint32_t v[kNW];
 #pragma unroll
-    for (int j = 0; j <= WPK; ++j)
-      if (ODD || j < WPK) v[j] = lds_u32(a + 4 * j);
+    for (int j = 0; j < kNW; ++j) v[j] = lds_u32(a + 4 * j);
 #pragma unroll
     for (int j = 0; j < WPK; ++j) {
       const int k = t * WPK + j;
       if (k >= C0 && k < C1) {
-        uint32_t x = ODD ? __funnelshift_r(v[j], v[j + 1], 16) : v[j];
-        if (j == WPK - 1) x &= last_mask;
-        w[k - C0] = x;
+        const int h0 = Win::off(2 * j) + (ODD ? 1 : 0);  // half-word index of element 2j
+        if (2 * j + 1 < Win::kKwc) {
+          const int h1 = Win::off(2 * j + 1) + (ODD ? 1 : 0);
+          const uint32_t lo_sel = (h0 & 1) ? 0x32u : 0x10u;
+          const uint32_t hi_sel = (h1 / 2 == h0 / 2) ? ((h1 & 1) ? 0x32u : 0x10u) : ((h1 & 1) ? 0x76u : 0x54u);
+          w[k - C0] = __byte_perm(v[h0 / 2], v[h1 / 2], lo_sel | (hi_sel << 8));
+        } else {
+          w[k - C0] = (h0 & 1) ? (v[h0 / 2] >> 16) : (v[h0 / 2] & 0xFFFFu);
+        }
       }
     }
   }
@@ -190,13 +209,16 @@ __device__ __forceinline__ void build_cols(uint32_t src, uint32_t e0, uint32_t t
   for (int c = 0; c < kN; c += 8) tmem_st_n<8>(abase + C0 + c, w + c);
 }
 
-template <int BN, int KH, int WPK>
+template <int BN, int KH, int KW, int CI, int DW>
 __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __grid_constant__ RowpackParams p) {
   using Cfg = RowpackCfg<BN>;
+  constexpr int WPK = TapWindow<KW, CI, DW>::kWpk;
   constexpr int kWords = (KH * WPK + 7) / 8 * 8;   // TMEM columns of one A buffer
   constexpr int kSteps = kWords / 8;               // K16 steps per plane
   constexpr int kHalfCols = (kSteps + 1) / 2 * 8;  // builder half 0: columns [0, kHalfCols), half 1: the rest
-  static_assert(kRpSlots * BN <= kRpACol && kRpACol + 2 * kWords <= 512, "TMEM budget");
+  // TMEM: p.nacc * BN accumulator columns, then p.nabuf A buffers (host: fits in 512)
+  const int nacc = p.nacc, nabuf = p.nabuf;
+  const uint32_t a_col = static_cast<uint32_t>(nacc * BN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -208,11 +230,11 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
   uint8_t* raw = epi + 2 * p.stage_bytes;
   uint64_t* rfull = reinterpret_cast<uint64_t*>(raw + static_cast<size_t>(S) * p.slot_bytes);
   uint64_t* rempty = rfull + S;
-  uint64_t* afull = rempty + S;       // [2]
-  uint64_t* afree = afull + 2;        // [2]
-  uint64_t* tfull = afree + 2;        // [kRpSlots]
-  uint64_t* tempty = tfull + kRpSlots;  // [kRpSlots]
-  uint64_t* bfull = tempty + kRpSlots;
+  uint64_t* afull = rempty + S;          // [kRpMaxA]
+  uint64_t* afree = afull + kRpMaxA;     // [kRpMaxA]
+  uint64_t* tfull = afree + kRpMaxA;     // [kRpMaxSlots]
+  uint64_t* tempty = tfull + kRpMaxSlots;  // [kRpMaxSlots]
+  uint64_t* bfull = tempty + kRpMaxSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
 
   if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
@@ -227,11 +249,11 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
       mbar_init(&rfull[i], 1);
       mbar_init(&rempty[i], 8);  // the 8 builder warps
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kRpMaxA; ++i) {
       mbar_init(&afull[i], 8);
       mbar_init(&afree[i], 1);
     }
-    for (int i = 0; i < kRpSlots; ++i) {
+    for (int i = 0; i < kRpMaxSlots; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 128);  // epilogue threads
     }
@@ -327,11 +349,10 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
                         static_cast<uint32_t>(p.shift + c * p.sw * p.ci);
     const uint32_t tap_step = static_cast<uint32_t>(p.dh) * static_cast<uint32_t>(p.box_w);
     const bool odd = (p.shift & 1) != 0;
-    const uint32_t last_mask = p.mask_last ? 0xFFFFu : 0xFFFFFFFFu;
-    const uint32_t lane_base = tmem_base + ((static_cast<uint32_t>(q) * 32u) << 16) + kRpACol;
+    const uint32_t lane_base = tmem_base + ((static_cast<uint32_t>(q) * 32u) << 16) + a_col;
     const uint32_t raw_s = smem_u32(raw);
     uint32_t slot = 0, phase = 0;
-    uint32_t pi = 0;  // plane counter (A buffer = pi & 1)
+    uint32_t pi = 0;  // plane counter (A buffer = pi % nabuf)
     for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
       for (int di = plane_lo; di <= plane_hi; ++di) {
         int o0, o1;
@@ -341,8 +362,8 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         const bool tr = trace && warp == 4 && lane == 0 && pi < 64;
         if (tr) trace[640 + 3 * pi] = clock64();
         const uint32_t src = raw_s + slot * static_cast<uint32_t>(p.slot_bytes);
-        const uint32_t ab = pi & 1, use = pi >> 1;
-        mbar_wait(&afree[ab], (use & 1) ^ 1);  // the MMAs of plane pi - 2 are done with buffer ab
+        const uint32_t ab = pi % nabuf, use = pi / nabuf;
+        mbar_wait(&afree[ab], (use & 1) ^ 1);  // the MMAs of plane pi - nabuf are done with buffer ab
         tc_fence_after();
         if (tr) trace[641 + 3 * pi] = clock64();
         const uint32_t abase = lane_base + ab * kWords;
@@ -353,11 +374,11 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           else
             for (int c0 = kHalfCols; c0 < kWords; c0 += 8) tmem_st_n<8>(abase + c0, z);
         } else if (half == 0) {
-          if (odd) build_cols<0, kHalfCols, KH, WPK, true>(src, e0, tap_step, last_mask, abase);
-          else build_cols<0, kHalfCols, KH, WPK, false>(src, e0, tap_step, last_mask, abase);
+          if (odd) build_cols<0, kHalfCols, KH, KW, CI, DW, true>(src, e0, tap_step, abase);
+          else build_cols<0, kHalfCols, KH, KW, CI, DW, false>(src, e0, tap_step, abase);
         } else {
-          if (odd) build_cols<kHalfCols, kWords, KH, WPK, true>(src, e0, tap_step, last_mask, abase);
-          else build_cols<kHalfCols, kWords, KH, WPK, false>(src, e0, tap_step, last_mask, abase);
+          if (odd) build_cols<kHalfCols, kWords, KH, KW, CI, DW, true>(src, e0, tap_step, abase);
+          else build_cols<kHalfCols, kWords, KH, KW, CI, DW, false>(src, e0, tap_step, abase);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&rempty[slot]);  // raw rows consumed (values are in TMEM / registers)
@@ -375,8 +396,8 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
     }
   } else if (warp == 13) {
     // ------------------------------------------------------------ MMA issuer
-    // Accumulators live in a ring of kRpSlots 64-column slots, one per output depth
-    // in flight (output depth g of the CTA's sequence -> slot g % kRpSlots): a
+    // Accumulators live in a ring of nacc BN-column slots, one per output depth
+    // in flight (output depth g of the CTA's sequence -> slot g % nacc): a
     // plane feeds up to ceil(KD/sd) depths, and the slot of a finished depth is
     // drained by the epilogue while the MMAs carry on with the next planes.
     const uint64_t b0 = smem_desc(smem_u32(sB), b_rows * Cfg::kBRowBytes, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
@@ -394,7 +415,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         int o0, o1;
         od_range(di, o0, o1);
         if (o0 > o1) continue;
-        const uint32_t ab = pi & 1, use = pi >> 1;
+        const uint32_t ab = pi % nabuf, use = pi / nabuf;
         mbar_wait(&afull[ab], use & 1);
         tc_fence_after();
         if (trace && lane == 0 && pi < 128) trace[256 + 2 * pi] = clock64();
@@ -402,10 +423,10 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           trace_event(p.trace, TR_FIRST_FULL);
           first_unit = false;
         }
-        const uint32_t a = tmem_base + kRpACol + ab * kWords;
+        const uint32_t a = tmem_base + a_col + ab * kWords;
         for (int od = o0; od <= o1; ++od) {
           const int g = ubase + od;
-          const uint32_t sl = static_cast<uint32_t>(g % kRpSlots), sph = static_cast<uint32_t>(g / kRpSlots) & 1u;
+          const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
           const int base = od * p.sd - p.pd;  // input plane of kd = 0
           const int kd = di - base;
           const bool first = di == (base > 0 ? base : 0);  // depth od's planes are contiguous
@@ -415,7 +436,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
             tc_fence_after();
           }
           if (elect_one()) {
-            const uint32_t d = tmem_base + kRpAccCol + sl * BN;
+            const uint32_t d = tmem_base + sl * BN;
             const uint64_t bk = b0 + static_cast<uint32_t>(kd) * kd_step;
 #pragma unroll
             for (int st = 0; st < kSteps; ++st)
@@ -450,7 +471,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
       decompose(u, n, th, tw);
       for (int od = 0; od < p.od; ++od) {
         const int g = ubase + od;
-        const uint32_t sl = static_cast<uint32_t>(g % kRpSlots), sph = static_cast<uint32_t>(g / kRpSlots) & 1u;
+        const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
         mbar_wait(&tfull[sl], sph);
         tc_fence_after();
         if (trace && threadIdx.x == 0 && ui < 64) trace[512 + 2 * ui] = clock64();
@@ -459,7 +480,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 32, ++chunk) {
           uint32_t r[32];
-          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + kRpAccCol + sl * BN + c0, r);
+          tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + sl * BN + c0, r);
           tmem_ld_wait();
           uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
           named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store

@@ -963,14 +963,14 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
 
 // ------------------------------------------------------------------ conv (rowpack, CI = 3 stems)
 
-template <int BN, int KH, int WPK>
+template <int BN, int KH, int KW, int CI, int DW>
 int launch_rowpack(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, WPK>,
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const DeviceInfo di = device_info();
   const int grid = std::min(p.total_units, di.sms);
   p.trace = g_trace;
-  CUDA_TRY(launch_pdl(tb::conv_rowpack_kernel<BN, KH, WPK>, grid, tb::kRpThreads, smem, stream, p));
+  CUDA_TRY(launch_pdl(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW>, grid, tb::kRpThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
 }
@@ -983,13 +983,17 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   if (tb::options().no_rowpack) return kNotEligible;
   if (g.transposed || g.g != 1 || epi.on()) return kNotEligible;
   if (g.co != 64 && g.co != 32) return kNotEligible;
-  if (g.d[2] != 1 || (g.s[2] * g.ci) % 2) return kNotEligible;  // one even-aligned (kw, c) run per tap
-  if (accumulate && Yin != Y) return kNotEligible;               // in-place accumulate = TMA reduce-add
+  if ((g.s[2] * g.ci) % 2) return kNotEligible;  // every lane's window starts at the same element parity
+  if (accumulate && Yin != Y) return kNotEligible;  // in-place accumulate = TMA reduce-add
   const int64_t kwc = g.k[2] * g.ci;
   const int64_t wpk = (kwc + 1) / 2;
   const int64_t KH = g.k[1];
-  // instantiated window shapes: 7 taps x 11 words (7x7 CI = 3), 3 taps x 5 words (3x3 CI = 3)
-  if (!((KH == 7 && wpk == 11) || (KH == 3 && wpk == 5))) return kNotEligible;
+  const int64_t span = (g.k[2] - 1) * g.d[2] * g.ci + g.ci;  // window elements first to last
+  // instantiated windows (KH x KW x CI, w-dilation): 7x7x3 (C3D, ResNet stem), 7x7x3 d2 (DIL), 3x3x3 (MobileNet stem)
+  const int shape = (g.ci == 3 && KH == 7 && g.k[2] == 7 && g.d[2] == 1) ? 0
+                    : (g.ci == 3 && KH == 7 && g.k[2] == 7 && g.d[2] == 2) ? 1
+                    : (g.ci == 3 && KH == 3 && g.k[2] == 3 && g.d[2] == 1) ? 2 : -1;
+  if (shape < 0) return kNotEligible;
   const int64_t kwords = (KH * wpk + 7) / 8 * 8;
   const int64_t kp = 2 * kwords;
   const int64_t OD = g.out[0], OH = g.out[1], OW = g.out[2];
@@ -1001,7 +1005,7 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   const int64_t tiles_w0 = (OW + Wt - 1) / Wt;
   if (tiles_w0 > 1 && (Wt * g.s[2] * g.ci) % 8) return kNotEligible;
   const int64_t shift = (8 - (g.p[2] * g.ci) % 8) % 8;
-  int64_t box_w = (shift + (Wt - 1) * g.s[2] * g.ci + 2 * wpk + 1 + 7) / 8 * 8;
+  int64_t box_w = (shift + (Wt - 1) * g.s[2] * g.ci + span + 2 + 7) / 8 * 8;
   // A warp's lanes cover two tile rows (Wt = 16): a row step of 16 (mod 32) words
   // keeps the builders' 32-bit shared loads conflict-free (lane c reads word 3c + ...)
   for (int64_t b = box_w; b <= box_w + 56 && b <= 256; b += 8) {
@@ -1014,7 +1018,14 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   if (box_w > 256 || box_h > 256) return kNotEligible;
   const int64_t wci = g.in[2] * g.ci;
   if ((wci * 2) % 16) return kNotEligible;  // TMA row pitch
-  if (g.d[0] != 1 || (g.k[0] + g.s[0] - 1) / g.s[0] > tb::kRpSlots - 1) return kNotEligible;  // depth window
+  // TMEM rings: ceil(KD/sd) depths in flight + one draining (>= 2: the epilogue of a
+  // tile overlaps the next tile's MMAs), then as many A buffers as fit (the builders
+  // run ahead of the MMAs by nabuf - 1 planes)
+  if (g.d[0] != 1) return kNotEligible;
+  const int64_t nacc = std::max<int64_t>(2, (g.k[0] + g.s[0] - 1) / g.s[0] + 1);
+  if (nacc > tb::kRpMaxSlots) return kNotEligible;
+  const int64_t nabuf = std::min<int64_t>(tb::kRpMaxA, (512 - nacc * g.co) / kwords);
+  if (nabuf < 2) return kNotEligible;
   const DeviceInfo di = device_info();
   const int bn = static_cast<int>(g.co);
   const int64_t b_bytes = g.k[0] * kp * bn * 2;
@@ -1106,14 +1117,20 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   p.shift = static_cast<int32_t>(shift);
   p.stages = stages;
   p.slot_bytes = slot_bytes;
-  p.mask_last = static_cast<int32_t>(kwc % 2);
   p.out_f16 = out_f16;
   p.store_mode = accumulate ? 2 : 1;
   p.stage_bytes = stage_bytes;
   p.debug = tb::options().rowpack_debug;
-  if (bn == 64)
-    return KH == 7 ? launch_rowpack<64, 7, 11>(p, smem, stream) : launch_rowpack<64, 3, 5>(p, smem, stream);
-  return KH == 7 ? launch_rowpack<32, 7, 11>(p, smem, stream) : launch_rowpack<32, 3, 5>(p, smem, stream);
+  p.nacc = static_cast<int32_t>(nacc);
+  p.nabuf = static_cast<int32_t>(nabuf);
+  if (bn == 64) {
+    if (shape == 0) return launch_rowpack<64, 7, 7, 3, 1>(p, smem, stream);
+    if (shape == 1) return launch_rowpack<64, 7, 7, 3, 2>(p, smem, stream);
+    return launch_rowpack<64, 3, 3, 3, 1>(p, smem, stream);
+  }
+  if (shape == 0) return launch_rowpack<32, 7, 7, 3, 1>(p, smem, stream);
+  if (shape == 1) return launch_rowpack<32, 7, 7, 3, 2>(p, smem, stream);
+  return launch_rowpack<32, 3, 3, 3, 1>(p, smem, stream);
 }
 
 int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,

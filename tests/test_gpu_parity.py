@@ -63,6 +63,8 @@ SMALL = {
     # 2-D stems: ResNet-50's 7x7 s2 and MobileNet-V2's 3x3 s2 (CI = 3)
     "C2D_stem7": tb.Conv("C2D", n=2, in_dhw=(1, 32, 32), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3)),
     "C2D_stem3": tb.Conv("C2D", n=2, in_dhw=(1, 24, 40), ci=3, co=32, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1)),
+    # rowpack with a dilated (kw, c) window (the DIL paper geometry on a small image)
+    "DIL_rp": tb.Conv("DIL", n=2, in_dhw=(1, 40, 48), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3), d=(1, 2, 2)),
     "DIL": tb.Conv("DIL", n=1, in_dhw=(1, 30, 30), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3), d=(1, 2, 2)),
     "DIL_ci64": tb.Conv("DIL", n=2, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), p=(0, 2, 2), d=(1, 2, 2)),
     "GRP": tb.Conv("GRP", n=2, in_dhw=(1, 12, 12), ci=64, co=128, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), groups=4),
@@ -110,7 +112,7 @@ def test_conv_d2_within_tolerance(name, cuda):
         assert O.tensors_bitwise_equal(got, want)
 
 
-@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D", "C3D_rp", "C2D_stem3"])
+@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D", "C3D_rp", "C2D_stem3", "DIL_rp"])
 def test_conv_accumulate_and_fp16_out(name, cuda):
     import torch
 
@@ -343,7 +345,7 @@ def kernels_launched(fn):
     return [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 
 
-@pytest.mark.parametrize("name", ["C3D_rp", "C3D_rp_odd", "C2D_stem7", "C2D_stem3"])
+@pytest.mark.parametrize("name", ["C3D_rp", "C3D_rp_odd", "C2D_stem7", "C2D_stem3", "DIL_rp"])
 def test_rowpack_vs_im2col_exact(name, option, cuda):
     """The rowpack kernel (default for these shapes: A operand packed in TMEM) and the
     (kw, c) relayout + im2col path (no_rowpack = 1) both equal the oracle bit for bit."""
