@@ -52,6 +52,8 @@ struct alignas(64) RowpackParams {
   int32_t stages, slot_bytes;
   int32_t out_f16, store_mode;  // store_mode 1: TMA store, 2: TMA reduce-add (Y += conv)
   int32_t stage_bytes;
+  const float* bias;  // fused epilogue (nullable): per-output-channel bias, then activation `act`
+  int32_t act;        // 0 none, 1 ReLU, 2 ReLU6, 3 GELU (epi_act)
   int32_t nacc, nabuf;  // TMEM rings: accumulator slots (<= kRpMaxSlots), A buffers (<= kRpMaxA)
   int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output stores
   unsigned long long* trace;
@@ -458,11 +460,16 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
     // order, tcgen05.ld 32 columns -> the pixel's line of a dense [R][Wt][32]
     // staging box (swizzled 16-byte chunks) -> one bulk tensor store per 32-column
     // chunk; double-buffered staging.
-    pdl_wait();  // Y may still be read by the preceding kernel
+    pdl_wait();  // Y (and the bias) may still be used / produced by the preceding kernel
     const uint32_t q = warp;
     const int m = static_cast<int>(q * 32 + lane);
     const bool mine = m < p.R * p.Wt;
     const int line_bytes = p.out_f16 ? 64 : 128;
+    // fused epilogue: lane j keeps bias[c0 + j] of each 32-column chunk (broadcast by shuffles)
+    float bias_lane[BN / 32];
+#pragma unroll
+    for (int i = 0; i < BN / 32; ++i) bias_lane[i] = p.bias ? __ldg(p.bias + 32 * i + lane) : 0.0f;
+    const bool epi_on = p.bias || p.act;
     uint32_t chunk = 0, ui = 0;
     int ubase = 0;
     bool first = true;
@@ -482,6 +489,15 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           uint32_t r[32];
           tmem_ld_32x32b_x32(tmem_base + ((q * 32u) << 16) + sl * BN + c0, r);
           tmem_ld_wait();
+          if (epi_on) {
+            float* v = reinterpret_cast<float*>(r);
+            if (p.bias) {
+              const float bl = bias_lane[c0 / 32];
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += __shfl_sync(0xffffffffu, bl, i);
+            }
+            epi_act_n<32>(v, p.act);
+          }
           uint8_t* buf = epi + (chunk & 1) * p.stage_bytes;
           named_bar_sync(1, 128);  // buffer (chunk & 1) no longer read by an older store
           if (mine) {

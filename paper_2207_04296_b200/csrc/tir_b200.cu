@@ -981,9 +981,10 @@ int launch_rowpack(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
 int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yin, void* Y,
                       int accumulate, int out_f16, const Epi& epi, cudaStream_t stream) {
   if (tb::options().no_rowpack) return kNotEligible;
-  if (g.transposed || g.g != 1 || epi.on()) return kNotEligible;
+  if (g.transposed || g.g != 1 || epi.residual) return kNotEligible;
   if (g.co != 64 && g.co != 32) return kNotEligible;
   if ((g.s[2] * g.ci) % 2) return kNotEligible;  // every lane's window starts at the same element parity
+  if (accumulate && epi.on()) return kNotEligible;  // the C-ABI order is (Yin + acc) + bias: not a reduce-add
   if (accumulate && Yin != Y) return kNotEligible;  // in-place accumulate = TMA reduce-add
   const int64_t kwc = g.k[2] * g.ci;
   const int64_t wpk = (kwc + 1) / 2;
@@ -1121,6 +1122,8 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   p.store_mode = accumulate ? 2 : 1;
   p.stage_bytes = stage_bytes;
   p.debug = tb::options().rowpack_debug;
+  p.bias = epi.bias;
+  p.act = epi.relu;
   p.nacc = static_cast<int32_t>(nacc);
   p.nabuf = static_cast<int32_t>(nabuf);
   if (bn == 64) {

@@ -77,7 +77,7 @@ def test_golden_vector_on_gpu(golden, name, cuda):
 
 
 EPI_CASES = ["C1D", "C2D", "C2D_ci96_co40", "C2D_ci8", "C3D", "DIL", "GRP", "GRP_g2", "T2D", "DEP",
-             "DEP_s2", "DEP_c12"]
+             "DEP_s2", "DEP_c12", "C3D_rp", "C2D_stem7", "C2D_stem3", "DIL_rp"]
 VARIANTS = [(True, False), (False, True), (True, True)]
 
 
@@ -102,7 +102,7 @@ def test_conv_epilogue_bit_exact(name, bias_on, relu, cuda):
     assert O.tensors_bitwise_equal(got.cpu().numpy(), want), name
 
 
-@pytest.mark.parametrize("name", ["C2D", "C2D_ci96_co40", "GRP", "T2D", "DEP", "DEP_c12"])
+@pytest.mark.parametrize("name", ["C2D", "C2D_ci96_co40", "GRP", "T2D", "DEP", "DEP_c12", "C2D_stem7", "C2D_stem3"])
 def test_conv_epilogue_with_accumulate_and_fp16(name, cuda):
     import torch
 
@@ -145,6 +145,32 @@ def test_gmm_epilogue_bit_exact(mnk, bias_on, relu, cuda):
     torch.cuda.synchronize()
     want = O.epilogue(O.gmm(a, b, c0, threads=8), bias if bias_on else None, relu)
     assert O.tensors_bitwise_equal(c.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("name,act", [("C2D_stem7", "relu"), ("C2D_stem3", "relu6"), ("C3D_rp", "gelu")])
+def test_rowpack_fused_stem_epilogue(name, act, cuda):
+    """The network stems' fused form on the rowpack kernel: bias + activation with
+    fp16 output, bit-exact against oracle.epilogue of the fp32 result, RN to fp16."""
+    import torch
+
+    spec = SMALL[name]
+    x, w, bias = _epi_inputs(spec, seed=7)
+    got = tb.conv(spec, dev(x, cuda), dev(w, cuda), bias=torch.from_numpy(bias).to(cuda), relu=act, out_f16=True)
+    torch.cuda.synchronize()
+    pre = O.epilogue(O.conv(ospec(spec), x, w, threads=8), bias)  # f32: conv + bias
+    got = got.float().cpu().numpy()
+    if act == "relu":
+        want = np.where(pre < 0, np.float32(0), pre)
+    elif act == "relu6":
+        want = np.minimum(np.where(pre < 0, np.float32(0), pre), np.float32(6))
+    else:  # erf GELU, float64 reference; the kernel's erf approximation is within 1.5e-7
+        from math import erf
+        want = np.vectorize(lambda v: 0.5 * v * (1.0 + erf(v / 2 ** 0.5)))(pre.astype(np.float64))
+    want = want.astype(np.float16).astype(np.float32)
+    if act == "gelu":
+        assert np.allclose(got, want, rtol=2 ** -10, atol=1e-3)
+    else:
+        assert np.array_equal(got, want)
 
 
 def test_epilogue_d2_relu_matches_sign_of_result(cuda):
