@@ -191,6 +191,7 @@ struct DepTileParams {
   int32_t accumulate, out_f16;
   const float* bias;  // fused epilogue (nullable)
   int32_t relu;
+  unsigned long long* trace;  // tools/cta_timeline.py milestones (nullable)
 };
 
 template <int K, int S, int R, int T, int TR, int TC, bool EPI>
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
                 oy0 * S - p.pad_h, n);
   };
 
+  if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
   if (threadIdx.x == 0) {
     prefetch_tmap(&p.tmX);  // descriptor fetch overlaps the prologue
     mbar_init(&bar[0], 1);
@@ -237,6 +239,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
   __syncthreads();
   pdl_launch_dependents();
   pdl_wait();
+  if (threadIdx.x == 0) trace_event(p.trace, TR_PDL_DONE);
   if (threadIdx.x == 0) {  // prime both ring slots
     if (static_cast<int>(blockIdx.x) < tiles) issue(blockIdx.x, 0);
     if (static_cast<int>(blockIdx.x + gridDim.x) < tiles) issue(blockIdx.x + gridDim.x, 1);
@@ -290,6 +293,7 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
       }
     if (slot == 0) { mbar_wait(&bar[0], phase0); phase0 ^= 1; }
     else { mbar_wait(&bar[1], phase1); phase1 ^= 1; }
+    if (k == 0 && threadIdx.x == 0) trace_event(p.trace, TR_FIRST_FULL);
     const __half* tile = reinterpret_cast<const __half*>(smem_raw + slot * kSlotBytes);
     const __half* my = tile + ((tr * R * S) * FC + tc * T * S) * CT + cv * 8;
 #pragma unroll
@@ -346,6 +350,10 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
           reinterpret_cast<float4*>(y)[1] = make_float4(f[2].x, f[2].y, f[3].x, f[3].y);
         }
       }
+  }
+  if (threadIdx.x == 0) {
+    trace_event(p.trace, TR_STORES_DONE);
+    trace_event(p.trace, TR_EXIT);
   }
 }
 

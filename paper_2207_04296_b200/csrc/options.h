@@ -27,6 +27,8 @@ struct Options {
   int ksplit = 0;          // > 0: force the split-K factor (cluster-reduced, deterministic)
   int no_halo = 0;         // 1: stride-1 convs take the im2col kernel
   int no_rowpack = 0;      // 1: CI = 3 stems / C3D take the (kw, c) relayout + im2col kernel
+  int rp_backoff = 64;     // rowpack: ns between barrier polls of producers / epilogue (0: spin)
+  int rp_backoff2 = 0;     // rowpack: same for the builders
   int rowpack_debug = 0;   // timing experiments only, WRONG results: 1 no raw loads in the builders, 2 no stores
   int pack_hw = -1;        // 0 / 1: disable / force the (kh, kw, c) relayout of CI % 8 != 0 layers
   int pack_kw = 1;         // 0: no (kw, c) relayout
@@ -54,6 +56,7 @@ inline const OptionEntry* option_table(int* count) {
       {"no_tma_store", &Options::no_tma_store}, {"bn", &Options::bn},
       {"ksplit", &Options::ksplit},         {"no_halo", &Options::no_halo},
       {"no_rowpack", &Options::no_rowpack},     {"rowpack_debug", &Options::rowpack_debug},
+      {"rp_backoff", &Options::rp_backoff},     {"rp_backoff2", &Options::rp_backoff2},
       {"pack_hw", &Options::pack_hw},       {"pack_kw", &Options::pack_kw},
       {"pack_gather", &Options::pack_gather}, {"dep_simple", &Options::dep_simple},
       {"dep_tc", &Options::dep_tc},         {"no_smem_bias", &Options::no_smem_bias},

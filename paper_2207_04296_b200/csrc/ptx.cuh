@@ -87,6 +87,22 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
   return ok != 0;
 }
 
+// Same, backing off with __nanosleep between polls: for waiters off the MMA
+// issue path, whose spinning try_waits would otherwise share the MIO queue with
+// the tcgen05.mma issue.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  const uint32_t addr = smem_u32(bar);
+  if (mbar_try_wait(addr, parity)) return;
+  uint64_t t0;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+  while (!mbar_try_wait(addr, parity)) {
+    __nanosleep(ns);
+    uint64_t t1;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    if (t1 - t0 > (1ull << 31)) __trap();
+  }
+}
+
 // Bounded wait: a pipeline bug must surface as a trapped kernel (an error the
 // host sees), never as a hung GPU. ~2^31 ns budget via %globaltimer.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -54,7 +54,7 @@ struct alignas(64) RowpackParams {
   int32_t stage_bytes;
   const float* bias;  // fused epilogue (nullable): per-output-channel bias, then activation `act`
   int32_t act;        // 0 none, 1 ReLU, 2 ReLU6, 3 GELU (epi_act)
-  int32_t nacc, nabuf;  // TMEM rings: accumulator slots (<= kRpMaxSlots), A buffers (<= kRpMaxA)
+  int32_t backoff_ns, backoff_ns2;  // poll back-off of producers / epilogue, and of the builders
   int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output stores
   unsigned long long* trace;
 };
@@ -211,16 +211,22 @@ __device__ __forceinline__ void build_cols(uint32_t src, uint32_t e0, uint32_t t
   for (int c = 0; c < kN; c += 8) tmem_st_n<8>(abase + C0 + c, w + c);
 }
 
-template <int BN, int KH, int KW, int CI, int DW>
+template <int BN, int KH, int KW, int CI, int DW, bool D3>
 __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __grid_constant__ RowpackParams p) {
   using Cfg = RowpackCfg<BN>;
   constexpr int WPK = TapWindow<KW, CI, DW>::kWpk;
   constexpr int kWords = (KH * WPK + 7) / 8 * 8;   // TMEM columns of one A buffer
   constexpr int kSteps = kWords / 8;               // K16 steps per plane
   constexpr int kHalfCols = (kSteps + 1) / 2 * 8;  // builder half 0: columns [0, kHalfCols), half 1: the rest
-  // TMEM: p.nacc * BN accumulator columns, then p.nabuf A buffers (host: fits in 512)
-  const int nacc = p.nacc, nabuf = p.nabuf;
-  const uint32_t a_col = static_cast<uint32_t>(nacc * BN);
+  // TMEM: nacc * BN accumulator columns, then nabuf A buffers. Compile-time, so the
+  // per-plane / per-depth ring arithmetic is multiply-shift, not division: 3-D
+  // convs keep ceil(KD/sd) <= 4 depths in flight + one draining, 2-D convs one
+  // tile computing + one draining; the A ring takes what is left (<= 4).
+  constexpr int nacc = D3 ? kRpMaxSlots : 2;
+  constexpr int nabuf_fit = (512 - nacc * BN) / kWords;
+  constexpr int nabuf = nabuf_fit < kRpMaxA ? nabuf_fit : kRpMaxA;
+  static_assert(nabuf >= 2, "TMEM budget");
+  constexpr uint32_t a_col = static_cast<uint32_t>(nacc * BN);
 
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -326,7 +332,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           if (o0 > o1) continue;
           if ((it & (kRpProducers - 1)) == pw) {
             const uint32_t slot = static_cast<uint32_t>(it % S), phase = static_cast<uint32_t>(it / S) & 1u;
-            mbar_wait(&rempty[slot], phase ^ 1);
+            mbar_wait_backoff(&rempty[slot], phase ^ 1, p.backoff_ns);
             if (trace && it < 128) trace[2 * it] = clock64();
             mbar_arrive_expect_tx(&rfull[slot], static_cast<uint32_t>(p.box_w * p.box_h * 2));
             tma_load_3d(raw + static_cast<size_t>(slot) * p.slot_bytes, &p.tmX, &rfull[slot], x0, y0,
@@ -360,12 +366,12 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         int o0, o1;
         od_range(di, o0, o1);
         if (o0 > o1) continue;
-        mbar_wait(&rfull[slot], phase);
+        mbar_wait_backoff(&rfull[slot], phase, p.backoff_ns2);
         const bool tr = trace && warp == 4 && lane == 0 && pi < 64;
         if (tr) trace[640 + 3 * pi] = clock64();
         const uint32_t src = raw_s + slot * static_cast<uint32_t>(p.slot_bytes);
         const uint32_t ab = pi % nabuf, use = pi / nabuf;
-        mbar_wait(&afree[ab], (use & 1) ^ 1);  // the MMAs of plane pi - nabuf are done with buffer ab
+        mbar_wait_backoff(&afree[ab], (use & 1) ^ 1, p.backoff_ns2);  // the MMAs of plane pi - nabuf are done with buffer ab
         tc_fence_after();
         if (tr) trace[641 + 3 * pi] = clock64();
         const uint32_t abase = lane_base + ab * kWords;
@@ -479,7 +485,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
       for (int od = 0; od < p.od; ++od) {
         const int g = ubase + od;
         const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
-        mbar_wait(&tfull[sl], sph);
+        mbar_wait_backoff(&tfull[sl], sph, p.backoff_ns);
         tc_fence_after();
         if (trace && threadIdx.x == 0 && ui < 64) trace[512 + 2 * ui] = clock64();
         if (first && threadIdx.x == 0) trace_event(p.trace, TR_FIRST_TFULL);

@@ -963,16 +963,22 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
 
 // ------------------------------------------------------------------ conv (rowpack, CI = 3 stems)
 
-template <int BN, int KH, int KW, int CI, int DW>
-int launch_rowpack(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW>,
+template <int BN, int KH, int KW, int CI, int DW, bool D3>
+int launch_rowpack_k(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
+  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW, D3>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
   const DeviceInfo di = device_info();
   const int grid = std::min(p.total_units, di.sms);
   p.trace = g_trace;
-  CUDA_TRY(launch_pdl(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW>, grid, tb::kRpThreads, smem, stream, p));
+  CUDA_TRY(launch_pdl(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW, D3>, grid, tb::kRpThreads, smem, stream, p));
   ++g_launches;
   return TIR_B200_OK;
+}
+
+template <int BN, int KH, int KW, int CI, int DW>
+int launch_rowpack(tb::RowpackParams& p, size_t smem, cudaStream_t stream, bool d3) {
+  return d3 ? launch_rowpack_k<BN, KH, KW, CI, DW, true>(p, smem, stream)
+            : launch_rowpack_k<BN, KH, KW, CI, DW, false>(p, smem, stream);
 }
 
 // Small-channel convolutions whose (kh, kw, c) window fits one TMEM K vector
@@ -1023,10 +1029,8 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   // tile overlaps the next tile's MMAs), then as many A buffers as fit (the builders
   // run ahead of the MMAs by nabuf - 1 planes)
   if (g.d[0] != 1) return kNotEligible;
-  const int64_t nacc = std::max<int64_t>(2, (g.k[0] + g.s[0] - 1) / g.s[0] + 1);
-  if (nacc > tb::kRpMaxSlots) return kNotEligible;
-  const int64_t nabuf = std::min<int64_t>(tb::kRpMaxA, (512 - nacc * g.co) / kwords);
-  if (nabuf < 2) return kNotEligible;
+  const bool d3 = g.k[0] > 1;  // 3-D: a ring of kRpMaxSlots depth accumulators (rowpack.cuh)
+  if (d3 && (g.k[0] + g.s[0] - 1) / g.s[0] + 1 > tb::kRpMaxSlots) return kNotEligible;
   const DeviceInfo di = device_info();
   const int bn = static_cast<int>(g.co);
   const int64_t b_bytes = g.k[0] * kp * bn * 2;
@@ -1122,18 +1126,18 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   p.store_mode = accumulate ? 2 : 1;
   p.stage_bytes = stage_bytes;
   p.debug = tb::options().rowpack_debug;
+  p.backoff_ns = tb::options().rp_backoff;
+  p.backoff_ns2 = tb::options().rp_backoff2;
   p.bias = epi.bias;
   p.act = epi.relu;
-  p.nacc = static_cast<int32_t>(nacc);
-  p.nabuf = static_cast<int32_t>(nabuf);
   if (bn == 64) {
-    if (shape == 0) return launch_rowpack<64, 7, 7, 3, 1>(p, smem, stream);
-    if (shape == 1) return launch_rowpack<64, 7, 7, 3, 2>(p, smem, stream);
-    return launch_rowpack<64, 3, 3, 3, 1>(p, smem, stream);
+    if (shape == 0) return launch_rowpack<64, 7, 7, 3, 1>(p, smem, stream, d3);
+    if (shape == 1) return launch_rowpack<64, 7, 7, 3, 2>(p, smem, stream, d3);
+    return launch_rowpack<64, 3, 3, 3, 1>(p, smem, stream, d3);
   }
-  if (shape == 0) return launch_rowpack<32, 7, 7, 3, 1>(p, smem, stream);
-  if (shape == 1) return launch_rowpack<32, 7, 7, 3, 2>(p, smem, stream);
-  return launch_rowpack<32, 3, 3, 3, 1>(p, smem, stream);
+  if (shape == 0) return launch_rowpack<32, 7, 7, 3, 1>(p, smem, stream, d3);
+  if (shape == 1) return launch_rowpack<32, 7, 7, 3, 2>(p, smem, stream, d3);
+  return launch_rowpack<32, 3, 3, 3, 1>(p, smem, stream, d3);
 }
 
 int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const float* Yin, void* Y,
@@ -1459,6 +1463,7 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   p.bias = epi.bias;
   p.relu = epi.relu;
   p.out_f16 = out_f16;
+  p.trace = g_trace;
   const int64_t blocks = g.n * p.tiles_h * p.tiles_w * p.cblocks;
   if (blocks >= (1ll << 31)) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: too many tiles");
   const size_t smem = 2 * ((static_cast<size_t>(FR) * FC * 32 * 2 + 127) / 128 * 128);  // two-slot ring

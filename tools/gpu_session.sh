@@ -1,3 +1,3 @@
-timeout 900 python -m pytest tests/test_gpu_epilogue.py tests/test_gpu_parity.py -m gpu -x -q 2>&1 | tail -3
-timeout 900 python -m pytest tests/test_gpu_nets.py -m gpu -x -q 2>&1 | tail -2
-timeout 600 python bench.py --no-ops --no-cpu --no-e2e 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print({k:(v.get('samples_per_s'), v.get('ms_per_forward')) for k,v in d['nets'].items()})"
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
+timeout 120 python tools/cta_timeline.py DEP 4 2>&1 | grep -v "^  block\|last 6" | head -8
+timeout 120 python tools/cta_timeline.py C2D 4 2>&1 | sed -n 2,3p

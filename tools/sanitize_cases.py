@@ -2,7 +2,7 @@
 (memcheck / racecheck / synccheck): igemm_tc_kernel (tiled GMM, im2col conv,
 T2D sub-pixel classes, cta_group::2 pairs, cluster split-K with the fused
 epilogue, batched attention GEMM), conv_halo_kernel, dep_tile_kernel and the
-untiled dep_kernel, the relayout kernels (channel pad, (kw, c) and
+untiled dep_kernel, conv_rowpack_kernel (C3D / DIL / fused stem), the relayout kernels (channel pad, (kw, c) and
 (kh, kw, c) packing), and the network glue (pooling, LayerNorm, softmax).
 Each result is checked so a sanitizer run also proves the launches computed.
 
@@ -53,10 +53,19 @@ cases = {
     "GRP": tb.Conv("GRP", n=1, in_dhw=(1, 8, 8), ci=64, co=64, k=(1, 3, 3), p=(0, 1, 1), groups=2),
     "DEP tile": tb.Conv("DEP", n=1, in_dhw=(1, 16, 32), ci=32, co=32, k=(1, 3, 3), p=(0, 1, 1), groups=32),
     "DEP simple": tb.Conv("DEP", n=1, in_dhw=(1, 7, 7), ci=12, co=12, k=(1, 5, 5), p=(0, 2, 2), groups=12),
+    # conv_rowpack_kernel: A operand packed in TMEM (7x7x3 window; w-dilated window; 3-D depth ring)
+    "C3D rowpack 7^3": tb.Conv("C3D", n=1, in_dhw=(7, 16, 24), ci=3, co=64, k=(7, 7, 7), s=(2, 2, 2), p=(3, 3, 3)),
+    "DIL rowpack d2": tb.Conv("DIL", n=1, in_dhw=(1, 24, 40), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3),
+                              d=(1, 2, 2)),
 }
 for name, spec in cases.items():
     x, w = rnd(*spec.x_shape()), rnd(*spec.w_shape())
     check(name, tb.conv(spec, x, w), ref_conv(spec, x, w))
+spec = tb.Conv("C2D", n=2, in_dhw=(1, 24, 40), ci=3, co=32, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1))
+x, w = rnd(*spec.x_shape()), rnd(*spec.w_shape())
+bias = torch.randn(32, device=dev, generator=g)
+check("stem rowpack + bias/ReLU6 fp16", tb.conv(spec, x, w, bias=bias, relu="relu6", out_f16=True),
+      ref_conv(spec, x, w).add(bias.double()).clamp(0, 6))
 spec = tb.Conv("T2D", n=1, in_dhw=(1, 4, 4), ci=64, co=64, k=(1, 4, 4), s=(1, 2, 2), p=(0, 1, 1), transposed=True)
 x, w = rnd(*spec.x_shape()), rnd(*spec.w_shape())
 y = tb.conv(spec, x, w)
