@@ -160,25 +160,30 @@ __global__ void __launch_bounds__(kHaloThreads, 1) conv_halo_kernel(const __grid
             if (p.l2_prefetch == 1 || box == static_cast<int>(blockIdx.x) / (p.groups * p.tiles_n))
               tma_prefetch_2d(&p.tmW, g * p.cog + nt * BN + ch * Cfg::kBChunk, r);
       }
-      // the first tile's decomposition and the loop constants before the wait
-      const uint32_t slab_tx = static_cast<uint32_t>(p.HR) * p.Wv * 128;
+      // the first tile's coordinates and every loop constant in registers before the
+      // wait (parameter loads after it miss the constant cache on the critical path)
+      const uint32_t slab_tx = static_cast<uint32_t>(pin(p.HR * p.Wv * 128));
+      const int R = pin(p.R), Wt = pin(p.Wt), pad_h = pin(p.pad_h), pad_w = pin(p.pad_w);
+      const int cblocks = pin(p.cblocks), cig = pin(p.cig), total = pin(p.total_tiles);
       uint32_t slot = 0, phase = 0;
       int it = 0;
-      bool weights_pending = static_cast<int>(blockIdx.x) < p.total_tiles;
+      bool weights_pending = static_cast<int>(blockIdx.x) < total;
       int n, th, tw, g, nt;
       decompose(blockIdx.x, n, th, tw, g, nt);
+      n = pin(n), th = pin(th), tw = pin(tw), g = pin(g);
       pdl_wait();  // X / W may be produced by the preceding kernel
       trace_event(p.trace, TR_PDL_DONE);
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      for (int tile = blockIdx.x; tile < total; tile += gridDim.x) {
         if (tile != static_cast<int>(blockIdx.x)) decompose(tile, n, th, tw, g, nt);
-        const int y0 = th * p.R - p.pad_h;
-        const int x0 = tw * p.Wt - p.pad_w;
-        for (int cb = 0; cb < p.cblocks; ++cb, ++it) {
+        const int y0 = th * R - pad_h;
+        const int x0 = tw * Wt - pad_w;
+        for (int cb = 0; cb < cblocks; ++cb, ++it) {
+          if (it == 0) trace_event(p.trace, TR_PRELOOP);
           mbar_wait(&empty[slot], phase ^ 1);
           if (trace && it < 128) trace[2 * it] = clock64();
           if (it == 0) trace_event(p.trace, TR_FIRST_ISSUE);
           mbar_arrive_expect_tx(&full[slot], slab_tx);
-          tma_load_4d(sA0 + slot * slab_bytes, &p.tmX, &full[slot], g * p.cig + cb * 64, x0, y0, n);
+          tma_load_4d(sA0 + slot * slab_bytes, &p.tmX, &full[slot], g * cig + cb * 64, x0, y0, n);
           if (trace && it < 128) trace[2 * it + 1] = clock64();
           if (weights_pending) {
             // Resident weights of this CTA's (group, n-tile) — grid % (groups*tiles_n)

@@ -484,6 +484,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       tmem_alloc(tmem_slot, Cfg::kTmemCols);
       tmem_relinquish();
     }
+    if (lane == 0) trace_event(p.trace, TR_PRELOOP);  // TMEM granted (tools/cta_timeline.py)
   }
   if (p.bias_floats) {
     pdl_wait();  // the bias may be produced by the preceding kernel
@@ -608,7 +609,6 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       const int4* ptab = pt.ptab;
       const int st0 = pt.st0, st1 = pt.st1;
       for (int st = st0; st < st1; ++st, ++it) {
-        if (it == 0 && pw == 0 && lane == 0) trace_event(p.trace, TR_PRELOOP);
         mbar_wait(&empty[slot], phase ^ 1);
         if (elect_one()) {
           if (trace && pw == 0 && it < 128) trace[2 * it] = clock64();

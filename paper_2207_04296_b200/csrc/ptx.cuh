@@ -27,6 +27,15 @@ __device__ __forceinline__ void sts_f32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v));
 }
 
+// Materialise a value in a register at this point of the program (the empty
+// volatile asm may not be moved across other volatile asm, e.g. griddepcontrol.wait):
+// kernel parameters read after a PDL wait can miss the constant cache (~0.4 us each on
+// the critical path, tools/cta_timeline.py), so producers pin the ones they need before it.
+__device__ __forceinline__ int pin(int v) {
+  asm volatile("" : "+r"(v));
+  return v;
+}
+
 __device__ __forceinline__ uint32_t warp_id() { return threadIdx.x >> 5; }
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31; }
 
