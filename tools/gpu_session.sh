@@ -1,10 +1,4 @@
-mkdir -p gpurun_out/s30
-timeout 900 python bench.py > gpurun_out/s30/bench.json 2> gpurun_out/s30/bench.err; echo "bench rc=$?"
-python - <<'PY'
-import json
-d=json.loads(open('gpurun_out/s30/bench.json').read().strip().splitlines()[-1])
-print('headline', d['value'], d['ms_per_step'], d['roofline'], d['clocks'])
-print('e2e', d['e2e']['value'], 'cpu', d['cpu_baseline']['value'])
-for k,o in d['ops'].items(): print(k, o['us'], o['tflops'], o['gbs'], o['frac_roofline'], o.get('frac_roofline_ex_floor'))
-print({k:(v.get('samples_per_s'), v.get('ms_per_forward')) for k,v in d['nets'].items()})
-PY
+for rep in 1 2; do for lib in ab/lib_base.so ab/lib_bnepi.so; do TIR_B200_LIB=$lib timeout 900 python bench.py --no-cpu --no-e2e --no-ops --nets bert_large 2>/dev/null | python -c "
+import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
+print('$lib', {k:v.get('samples_per_s') for k,v in d['nets'].items()})"; done; done
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
