@@ -548,8 +548,11 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
       }
     }
     if (threadIdx.x == 0) {
-      tma_store_wait_all<0>();
-      trace_event(p.trace, TR_STORES_DONE);
+      tma_store_wait_read<0>();  // smem reads done; the grid end flushes the writes
+      if (p.trace) {
+        tma_store_wait_all<0>();  // (trace only) the stores themselves complete
+        trace_event(p.trace, TR_STORES_DONE);
+      }
     }
   }
 

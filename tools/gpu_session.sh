@@ -1,4 +1,3 @@
-for rep in 1 2; do for lib in ab/lib_base.so ab/lib_bnepi.so; do TIR_B200_LIB=$lib timeout 900 python bench.py --no-cpu --no-e2e --no-ops --nets bert_large 2>/dev/null | python -c "
-import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1])
-print('$lib', {k:v.get('samples_per_s') for k,v in d['nets'].items()})"; done; done
-timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -1
+for rep in 1 2 3; do for lib in ab/lib_base2.so ab/lib_wr.so; do for op in C2D DIL; do
+TIR_B200_LIB=$lib timeout 300 python bench.py --op $op --no-ops --no-cpu --no-e2e --no-nets --steps 200 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$lib', '$op', round(d['ms_per_step']*1e3,3))"
+done; done; done
