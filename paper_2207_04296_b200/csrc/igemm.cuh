@@ -122,6 +122,7 @@ struct alignas(64) IgemmParams {
                         // boxes {64 K, BN rows} (attention's Q K^T reads K straight from QKV)
   int32_t mc;           // 2: cta_group::2 CTA pair (CG2 instantiation, clusters of 2): see mc_tile
   int32_t batch_z2;     // problems per z1
+  int32_t gp_taps, gp_kpg;  // GP instantiation (group-packed): taps, K16 steps per packed group (cig / 16)
   BatchAxis ba, bb, bc; // A / B / C coordinates per problem
 };
 
@@ -148,7 +149,12 @@ __device__ __forceinline__ int batch_col(const BatchAxis& a, int z1, int z2) {
 // lane quadrant, alternating column chunks — so two epilogue warps share each
 // SM sub-partition and overlap their latency-bound chunk chains; 3 producers
 // suffice for one or two stages per tile.
-template <int BN, int KS, bool EPI8 = false>
+// GP (group-packed): a 64-channel im2col piece carries 64 / cig groups of a grouped
+// conv (cig = 16 or 32); the tile's BN columns are those groups' 32 output columns
+// each, every MMA is N = 32 on its group's K16 steps, B is the [taps*cig, 32] panel
+// of each group (32-column SW64 chunks). One TMA request per tap feeds all the
+// packed groups instead of one narrow request per group.
+template <int BN, int KS, bool EPI8 = false, bool GP = false>
 struct IgemmCfg {
   static constexpr int kEpiWarps = EPI8 ? 8 : 4;
   static constexpr int kProd = EPI8 ? 3 : 4;
@@ -161,10 +167,10 @@ struct IgemmCfg {
   static constexpr int kNacc = (4 * BN <= 512) ? 4 : 2;     // TMEM accumulator buffers
   static constexpr int kTmemCols = (kNacc * BN <= 32) ? 32 : (kNacc * BN <= 64) ? 64
                                    : (kNacc * BN <= 128) ? 128 : (kNacc * BN <= 256) ? 256 : 512;
-  static constexpr int kBChunk = BN < 64 ? BN : 64;        // columns per B TMA box
+  static constexpr int kBChunk = GP ? 32 : BN < 64 ? BN : 64;  // columns per B TMA box
   static constexpr int kBRowBytes = kBChunk * 2;           // 128 / 64 / 32
   static constexpr uint32_t kBLayout = kBRowBytes == 128 ? 2u : kBRowBytes == 64 ? 4u : 6u;
-  static constexpr uint32_t kIdesc = idesc_f16_f32(kBM, BN, /*A K-major*/ 0, /*B MN-major*/ 1);
+  static constexpr uint32_t kIdesc = idesc_f16_f32(kBM, GP ? 32 : BN, /*A K-major*/ 0, /*B MN-major*/ 1);
   // epilogue staging: per epilogue warp two 4 KB buffers (32 rows x 32 fp32)
   static constexpr int kEpiWarpBytes = 8192;
   static constexpr int kEpiBytes = kEpiWarps * kEpiWarpBytes;
@@ -422,10 +428,10 @@ __device__ __forceinline__ int4 make_piece(const IgemmParams& p, const SubProb& 
 
 // CG2 instantiations (host p.mc == 2) contain cta_group::2 instructions and must be
 // launched as clusters of 2; every other launch uses CG2 = false.
-template <int BN, int KS, bool EPI8 = false, bool CG2 = false>
+template <int BN, int KS, bool EPI8 = false, bool CG2 = false, bool GP = false>
 __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     igemm_tc_kernel(const __grid_constant__ IgemmParams p) {
-  using Cfg = IgemmCfg<BN, KS, EPI8>;
+  using Cfg = IgemmCfg<BN, KS, EPI8, GP>;
   constexpr int kProducers = Cfg::kProd;
   constexpr int kEpi = Cfg::kEpiWarps;
   extern __shared__ uint8_t smem_raw[];
@@ -590,12 +596,19 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
       __syncwarp();
       if (elect_one()) {
-        for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)
+        if constexpr (GP) {
+          // one box of all b_res_rows rows per packed group's 32 columns
+          for (int ch = pw; ch < kBChunks; ch += kProducers)
+            tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes, &p.tmB, bres_full,
+                        col0 + ch * Cfg::kBChunk, 0);
+        } else {
+          for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)
 #pragma unroll
-          for (int ch = 0; ch < kBChunks; ++ch)
-            tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
-                            static_cast<size_t>(r) * Cfg::kBRowBytes,
-                        &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
+            for (int ch = 0; ch < kBChunks; ++ch)
+              tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
+                              static_cast<size_t>(r) * Cfg::kBRowBytes,
+                          &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
+        }
       }
       __syncwarp();
     }
@@ -745,6 +758,26 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         const uint64_t a = adesc0 + slot * kAslot;
         const uint64_t b = bdesc0 + (b_res ? st * kBst : slot * kBslot);
         if (elect_one()) {
+          if constexpr (GP) {
+            // sub-block u = tap st*KS + u (one 64-channel piece); K16 step k of it is
+            // packed group k / kpg's step k % kpg; its B rows are that group's
+            // [tap*cig + 16*(k % kpg), +16) of its own 32-column chunk
+            const int kpg = p.gp_kpg;
+            const uint32_t kBgrp = static_cast<uint32_t>(p.b_res_rows * Cfg::kBRowBytes) >> 4;
+#pragma unroll
+            for (int u = 0; u < KS; ++u) {
+              const int t = st * KS + u;
+              if (t >= p.gp_taps) continue;  // K padding of the last stage
+#pragma unroll
+              for (int k = 0; k < kBK / 16; ++k) {
+                const int q = kpg == 1 ? k : k >> 1, kk = k - q * kpg;
+                const uint32_t brow = static_cast<uint32_t>((t * kpg + kk) * 16);
+                umma_f16(tmem_d + q * 32, a + u * kAsub + (a_koff[k] >> 4),
+                         bdesc0 + q * kBgrp + ((brow * Cfg::kBRowBytes) >> 4), Cfg::kIdesc,
+                         (st != st0 || u != 0 || kk != 0) ? 1u : 0u);
+              }
+            }
+          } else {
 #pragma unroll
           for (int u = 0; u < KS; ++u)
 #pragma unroll
@@ -756,6 +789,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
                 umma_f16(tmem_d, a + u * kAsub + (a_koff[k] >> 4), b + u * kBsub + k * kBk,
                          idesc, ((st - st0) | u | k) != 0);
             }
+          }  // !GP
           if constexpr (cg2) umma_commit_cg2(&empty[slot]);
           else umma_commit(&empty[slot]);
         }

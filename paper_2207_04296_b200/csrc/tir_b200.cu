@@ -277,6 +277,8 @@ cudaError_t launch_pdl_cluster(void (*kernel)(Params), int grid, int cluster, in
 // Measured on B200, vs unpaired: 8192^3 1094 -> 1290 TFLOPS, BERT-large QKV /
 // FFN1 / FFN2 GEMMs -11 / -12 / -15 %. (A B-multicast-only pair was measured
 // too: +4-7 % at 8192^3, nothing below; removed.) TIR_B200_MC=0 disables pairs.
+constexpr int kNotEligible = -100;  // a specialised path declines; the caller takes the general one
+
 bool use_pairs(const tb::IgemmParams& p, int bn) {
   if (!tb::options().mc) return false;
   return p.a_mode == tb::A_TILED && p.b_mode == tb::B_STREAM && !p.b_kmajor && p.num_sub == 1 &&
@@ -284,9 +286,9 @@ bool use_pairs(const tb::IgemmParams& p, int bn) {
          p.total_tiles == p.sub[0].tiles_m * p.tiles_n;
 }
 
-template <int BN, int KS, bool EPI8>
+template <int BN, int KS, bool EPI8, bool GP = false>
 int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
-  using Cfg = tb::IgemmCfg<BN, KS, EPI8>;
+  using Cfg = tb::IgemmCfg<BN, KS, EPI8, GP>;
   const DeviceInfo di = device_info();
   const int table = p.total_pieces * 16;
   // Stage the bias in shared memory for the TMA-store epilogue when it is small
@@ -307,7 +309,8 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   int nst_max = 0;
   for (int i = 0; i < p.num_sub; ++i) nst_max = std::max(nst_max, p.sub[i].num_stages);
   const int keys = p.groups * p.tiles_n * p.ksplit;  // CTAs per B-panel cycle
-  const int res_rows = nst_max * Cfg::kBRows;
+  // GP: the panel is the packed groups' own [taps*cig, 32] blocks (not stage-padded)
+  const int res_rows = GP ? p.gp_taps * p.gp_kpg * 16 : nst_max * Cfg::kBRows;
   const int res_bytes = res_rows * BN * 2;
   int grid = std::min(p.total_tiles, di.sms);
   // Keep B resident when its whole K panel fits next to a >= 3-deep A ring and
@@ -319,6 +322,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     p.stages = std::min(8, (budget - res_bytes) / Cfg::kABytes);
     grid = std::min(p.total_tiles, di.sms / keys * keys);
   } else {
+    if (GP) return kNotEligible;  // GP reads its panel resident only
     p.b_res_rows = 0;
     p.stages = std::min(8, budget / (Cfg::kABytes + Cfg::kBBytes));
   }
@@ -342,6 +346,17 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     ++g_launches;
     return TIR_B200_OK;
   }
+  if constexpr (GP) {
+    if (p.ksplit != 1) return kNotEligible;
+    CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8, false, true>,
+                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (const int e = tb::options().max_ctas) grid = std::max(1, std::min(grid, e));
+    p.mc = 0;
+    p.trace = g_trace;
+    CUDA_TRY(launch_pdl(tb::igemm_tc_kernel<BN, KS, EPI8, false, true>, grid, Cfg::kThreadsN, smem, stream, p));
+    ++g_launches;
+    return TIR_B200_OK;
+  } else {
   CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(smem)));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
@@ -389,6 +404,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   }
   ++g_launches;
   return TIR_B200_OK;
+  }  // !GP
 }
 
 // Short-K tiles (<= 1024-deep reduction, no split-K) with a wide, fused fp16 /
@@ -418,6 +434,14 @@ int launch_igemm_ks(tb::IgemmParams& p, int ks, cudaStream_t stream) {
     case 2: return e8 ? launch_igemm_bn<BN, 2, true>(p, stream) : launch_igemm_bn<BN, 2, false>(p, stream);
     default: return e8 ? launch_igemm_bn<BN, 1, true>(p, stream) : launch_igemm_bn<BN, 1, false>(p, stream);
   }
+}
+
+int launch_igemm_gp(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
+  if (bn == 128) return ks >= 2 ? launch_igemm_bn<128, 2, false, true>(p, stream)
+                                : launch_igemm_bn<128, 1, false, true>(p, stream);
+  if (bn == 64) return ks >= 2 ? launch_igemm_bn<64, 2, false, true>(p, stream)
+                               : launch_igemm_bn<64, 1, false, true>(p, stream);
+  return kNotEligible;
 }
 
 int launch_igemm(tb::IgemmParams& p, int bn, int ks, cudaStream_t stream) {
@@ -811,7 +835,6 @@ int pick_box(int64_t cig) {
 
 // ------------------------------------------------------------------ conv (halo, stride 1)
 
-constexpr int kNotEligible = -100;  // halo path declines; caller uses im2col
 
 template <int BN, int KH, int KW>
 int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
@@ -1292,6 +1315,23 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
   p.out_f16 = out_f16;
   p.Y = Y;
   p.Yin = Yin;
+  // Group packing (igemm.cuh GP): 64 / cig groups of 16 or 32 input channels share
+  // one 64-channel im2col piece per tap (one TMA request instead of 64 / cig narrow
+  // ones), each group an N = 32 MMA into its own accumulator columns.
+  int gp = 1;
+  if (!g.transposed && g.g > 1 && (cig == 16 || cig == 32) && cog == 32 && g.g % (64 / cig) == 0 &&
+      taps * cig <= 256 && !tb::options().no_gpack)
+    gp = static_cast<int>(64 / cig);
+  if (gp > 1) {
+    p.groups = static_cast<int32_t>(g.g / gp);
+    p.a_box_ch = 64;
+    p.cig = 64;
+    p.cb_per_tap = 1;
+    p.k_rows = static_cast<int32_t>(taps * 64);
+    p.cog = 32 * gp;
+    p.gp_taps = static_cast<int32_t>(taps);
+    p.gp_kpg = static_cast<int32_t>(cig / 16);
+  }
   epi.apply(p);
 
   const int lim_off = offset_limit(rank);
@@ -1323,17 +1363,27 @@ int conv_tc_impl(const Geo& g0, const uint16_t* X0, const uint16_t* W0, const fl
     }
     s.num_pieces = static_cast<int32_t>(taps * p.cb_per_tap);
     p.b_mode = tb::B_STREAM;
-    int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, box);
+    int rc = encode_im2col(&p.tmA[0], X, g, g.ci, rank, lower, upper, estr, p.a_box_ch);
     if (rc) return rc;
-    const int bn = choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, taps * ((cig + 15) / 16), di.sms,
-                             !out_f16 && !epi.on());
-    int ks = choose_ks(s.num_pieces, box, bn);
+    const int bn = gp > 1 ? p.cog
+                          : choose_bn(cog, (M + tb::kBM - 1) / tb::kBM, g.g, taps * ((cig + 15) / 16), di.sms,
+                                      !out_f16 && !epi.on());
+    int ks = choose_ks(s.num_pieces, p.a_box_ch, bn);
     if (bn >= 128) ks = std::min(ks, 2);
-    rc = encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK * ks);
+    // GP: B is read as each packed group's [taps*cig, 32] block, one box per group
+    rc = gp > 1 ? encode_2d(&p.tmB, W, taps * cig, g.co, 32, static_cast<int>(taps * cig))
+                : encode_2d(&p.tmB, W, taps * cig, g.co, std::min(bn, 64), tb::kBK * ks);
     if (rc) return rc;
     p.ksplit = 1;
     rc = finalize_tiles(p, bn, ks);
     if (rc) return rc;
+    if (gp > 1) {
+      rc = pick_store_mode(p, bn, Y, Yin, M, accumulate, out_f16);
+      if (rc) return rc;
+      rc = launch_igemm_gp(p, bn, ks, stream);
+      if (rc != kNotEligible) return rc;
+      return set_err(TIR_B200_ERR_UNSUPPORTED, "grouped conv: packed plan does not fit");
+    }
     p.ksplit = choose_ksplit(p, p.total_tiles, out_f16, di.sms);
     if (p.ksplit > 1) {
       rc = finalize_tiles(p, bn, ks);

@@ -1,3 +1,2 @@
-for rep in 1 2 3; do for lib in ab/lib_base2.so ab/lib_wr.so; do for op in C2D DIL; do
-TIR_B200_LIB=$lib timeout 300 python bench.py --op $op --no-ops --no-cpu --no-e2e --no-nets --steps 200 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('$lib', '$op', round(d['ms_per_step']*1e3,3))"
-done; done; done
+for e in 0 1; do TIR_B200_EPI8=$e timeout 300 python bench.py --op GRP --no-ops --no-cpu --no-e2e --no-nets --steps 200 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('GRP epi8=$e', round(d['ms_per_step']*1e3,3))"; done
+TIR_B200_EPI8=1 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -x -q -k "GRP" 2>&1 | tail -1
