@@ -34,7 +34,8 @@
 namespace tb {
 
 constexpr int kRpProducers = 4;   // TMA producer warps (raw boxes of planes it = pw mod 4)
-constexpr int kRpThreads = 544;  // warps 0-3 epilogue, 4-11 builders, 12 + 14-16 producers, 13 MMA
+constexpr int kRpThreads = 544;  // warps 0-3 epilogue, 4-11 builders, 12 MMA, 13-16 producers
+constexpr int kRpMmaWarp = 12;   // on SM sub-partition 0 (warp % 4 == 0)
 constexpr int kRpMaxSlots = 5;   // TMEM accumulator ring (p.nacc slots): output depths in flight + one draining
 constexpr int kRpMaxA = 4;       // TMEM A-buffer ring (p.nabuf buffers of KWORDS columns after the accumulators)
 
@@ -55,7 +56,8 @@ struct alignas(64) RowpackParams {
   const float* bias;  // fused epilogue (nullable): per-output-channel bias, then activation `act`
   int32_t act;        // 0 none, 1 ReLU, 2 ReLU6, 3 GELU (epi_act)
   int32_t backoff_ns, backoff_ns2;  // poll back-off of producers / epilogue, and of the builders
-  int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output stores
+  int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output
+                  // stores, 4 no A build at all
   unsigned long long* trace;
 };
 
@@ -247,7 +249,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
 
   if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
   const uint32_t warp = warp_id(), lane = lane_id();
-  if (threadIdx.x == 32 * 12 + 1) {
+  if (threadIdx.x == 32 * 13 + 1) {
     prefetch_tmap(&p.tmX);
     prefetch_tmap(&p.tmB);
     prefetch_tmap(&p.tmY);
@@ -268,7 +270,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
     mbar_init(bfull, 1);
     fence_barrier_init();
   }
-  if (warp == 13) {
+  if (warp == kRpMmaWarp) {
     tmem_alloc(tmem_slot, 512);
     tmem_relinquish();
   }
@@ -303,11 +305,11 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
     if (o1 > p.od - 1) o1 = p.od - 1;
   };
 
-  if (warp == 12 || warp >= 14) {
+  if (warp >= 13) {
     // ------------------------------------------------------------ producers
     // One raw box (box_h short rows) per plane; a TMA issue costs an issuing warp
     // ~1000+ cycles for such a box, so 4 producer warps take planes it = pw (mod 4).
-    const int pw = warp == 12 ? 0 : static_cast<int>(warp) - 13;
+    const int pw = static_cast<int>(warp) - 13;
     if (elect_one()) {
       pdl_wait();  // X / W may be produced by the preceding kernels
       if (pw == 0) {
@@ -375,7 +377,9 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         tc_fence_after();
         if (tr) trace[641 + 3 * pi] = clock64();
         const uint32_t abase = lane_base + ab * kWords;
-        if (p.debug & 1) {
+        if (p.debug & 4) {
+          // timing experiment: no A build at all (stale TMEM)
+        } else if (p.debug & 1) {
           uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
           if (half == 0)
             for (int c0 = 0; c0 < kHalfCols; c0 += 8) tmem_st_n<8>(abase + c0, z);
@@ -402,7 +406,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         }
       }
     }
-  } else if (warp == 13) {
+  } else if (warp == kRpMmaWarp) {
     // ------------------------------------------------------------ MMA issuer
     // Accumulators live in a ring of nacc BN-column slots, one per output depth
     // in flight (output depth g of the CTA's sequence -> slot g % nacc): a
@@ -432,29 +436,29 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           first_unit = false;
         }
         const uint32_t a = tmem_base + a_col + ab * kWords;
-        for (int od = o0; od <= o1; ++od) {
-          const int g = ubase + od;
-          const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
-          const int base = od * p.sd - p.pd;  // input plane of kd = 0
-          const int kd = di - base;
-          const bool first = di == (base > 0 ? base : 0);  // depth od's planes are contiguous
-          const bool last = di == (base + p.kd - 1 < p.d - 1 ? base + p.kd - 1 : p.d - 1);
-          if (first) {
-            mbar_wait(&tempty[sl], sph ^ 1);
-            tc_fence_after();
-          }
-          if (elect_one()) {
+        // one elected thread issues the whole plane (no per-depth warp reconvergence)
+        if (elect_one()) {
+          for (int od = o0; od <= o1; ++od) {
+            const int g = ubase + od;
+            const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
+            const int base = od * p.sd - p.pd;  // input plane of kd = 0
+            const int kd = di - base;
+            const bool first = di == (base > 0 ? base : 0);  // depth od's planes are contiguous
+            const bool last = di == (base + p.kd - 1 < p.d - 1 ? base + p.kd - 1 : p.d - 1);
+            if (first) {
+              mbar_wait(&tempty[sl], sph ^ 1);
+              tc_fence_after();
+            }
             const uint32_t d = tmem_base + sl * BN;
             const uint64_t bk = b0 + static_cast<uint32_t>(kd) * kd_step;
 #pragma unroll
             for (int st = 0; st < kSteps; ++st)
               umma_f16_ts(d, a + 8 * st, bk + st * kBk16, Cfg::kIdesc, (first && st == 0) ? 0u : 1u);
             if (last) umma_commit(&tfull[sl]);
+            if (trace && pi < 48 && od - o0 < 4) trace[832 + 4 * pi + (od - o0)] = clock64();
           }
-          __syncwarp();
-          if (trace && lane == 0 && pi < 48 && od - o0 < 4) trace[832 + 4 * pi + (od - o0)] = clock64();
+          umma_commit(&afree[ab]);
         }
-        if (elect_one()) umma_commit(&afree[ab]);
         __syncwarp();
         if (trace && lane == 0 && pi < 128) trace[257 + 2 * pi] = clock64();
         ++pi;
@@ -559,7 +563,7 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 13) tmem_dealloc(tmem_base, 512);
+  if (warp == kRpMmaWarp) tmem_dealloc(tmem_base, 512);
   if (threadIdx.x == 0) trace_event(p.trace, TR_EXIT);
 }
 
