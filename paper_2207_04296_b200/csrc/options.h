@@ -37,6 +37,7 @@ struct Options {
   int dep_simple = 0;      // 1: DEP takes the untiled kernel
   int dep_tc = 0;          // 8 / 16: DEP stride-1 tile-width override
   int no_smem_bias = 0;    // 1: never stage the bias in shared memory
+  int host_chunks = 8;     // host-buffer calls: batch chunks of the H2D / conv / D2H pipeline
   int host_pipeline = 1;   // 0: host-buffer calls do not pipeline batch chunks
   int l2_prefetch = 2;     // 0: the halo conv does not prefetch its first tile into L2 before the PDL
                            // wait; 1: it also prefetches the whole weight panel (2: one box per CTA) (measured: the same prefetch in igemm / DEP cost 0.7-1.7 us — the
@@ -61,7 +62,8 @@ inline const OptionEntry* option_table(int* count) {
       {"pack_hw", &Options::pack_hw},       {"pack_kw", &Options::pack_kw},
       {"pack_gather", &Options::pack_gather}, {"dep_simple", &Options::dep_simple},
       {"dep_tc", &Options::dep_tc},         {"no_smem_bias", &Options::no_smem_bias},
-      {"host_pipeline", &Options::host_pipeline}, {"l2_prefetch", &Options::l2_prefetch},
+      {"host_pipeline", &Options::host_pipeline},
+      {"host_chunks", &Options::host_chunks}, {"l2_prefetch", &Options::l2_prefetch},
   };
   *count = static_cast<int>(sizeof t / sizeof t[0]);
   return t;

@@ -64,10 +64,85 @@ using EncodeIm2colFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_
                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
 
 struct Driver {
-  EncodeTiledFn tiled = nullptr;
+  EncodeTiledFn tiled = nullptr;   // the caching wrappers below
   EncodeIm2colFn im2col = nullptr;
   int version = 0;
 };
+
+EncodeTiledFn g_encode_tiled = nullptr;   // the driver's entry points
+EncodeIm2colFn g_encode_im2col = nullptr;
+
+// Tensor-map encodes are a few microseconds of host time each and a call plans
+// 2-3 of them; repeated calls on the same buffers (graph capture loops, the
+// host-buffer pipeline's per-chunk launches) re-encode identical maps. A small
+// per-thread cache keyed by every encode argument returns the previous result.
+struct EncodeKey {
+  uint64_t w[40];
+  int n = 0;
+  void put(uint64_t v) { w[n++] = v; }
+  bool operator==(const EncodeKey& o) const { return n == o.n && std::memcmp(w, o.w, n * sizeof(uint64_t)) == 0; }
+};
+struct EncodeCache {
+  static constexpr int kSize = 32;
+  EncodeKey key[kSize];
+  CUtensorMap map[kSize];
+  int next = 0;
+  bool find(const EncodeKey& k, CUtensorMap* out) const {
+    for (int i = 0; i < kSize; ++i)
+      if (key[i] == k) {
+        *out = map[i];
+        return true;
+      }
+    return false;
+  }
+  void put(const EncodeKey& k, const CUtensorMap& m) {
+    key[next] = k;
+    map[next] = m;
+    next = (next + 1) % kSize;
+  }
+};
+thread_local EncodeCache t_encode_cache;
+
+CUresult encode_tiled_cached(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr,
+                             const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                             const cuuint32_t* es, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                             CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+  EncodeKey k;
+  k.put(1);
+  k.put(dt);
+  k.put(rank);
+  k.put(reinterpret_cast<uintptr_t>(ptr));
+  for (cuuint32_t i = 0; i < rank; ++i) k.put(dims[i]);
+  for (cuuint32_t i = 0; i + 1 < rank; ++i) k.put(strides[i]);
+  for (cuuint32_t i = 0; i < rank; ++i) k.put((static_cast<uint64_t>(box[i]) << 32) | es[i]);
+  k.put((static_cast<uint64_t>(il) << 48) | (static_cast<uint64_t>(sw) << 32) | (static_cast<uint64_t>(l2) << 16) | oob);
+  if (t_encode_cache.find(k, m)) return CUDA_SUCCESS;
+  const CUresult r = g_encode_tiled(m, dt, rank, ptr, dims, strides, box, es, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) t_encode_cache.put(k, *m);
+  return r;
+}
+
+CUresult encode_im2col_cached(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr,
+                              const cuuint64_t* dims, const cuuint64_t* strides, const int* lo, const int* hi,
+                              cuuint32_t ch, cuuint32_t px, const cuuint32_t* es, CUtensorMapInterleave il,
+                              CUtensorMapSwizzle sw, CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob) {
+  EncodeKey k;
+  k.put(2);
+  k.put(dt);
+  k.put(rank);
+  k.put(reinterpret_cast<uintptr_t>(ptr));
+  for (cuuint32_t i = 0; i < rank; ++i) k.put(dims[i]);
+  for (cuuint32_t i = 0; i + 1 < rank; ++i) k.put(strides[i]);
+  for (cuuint32_t i = 0; i + 2 < rank; ++i)
+    k.put((static_cast<uint64_t>(static_cast<uint32_t>(lo[i])) << 32) | static_cast<uint32_t>(hi[i]));
+  k.put((static_cast<uint64_t>(ch) << 32) | px);
+  for (cuuint32_t i = 0; i < rank; ++i) k.put(es[i]);
+  k.put((static_cast<uint64_t>(il) << 48) | (static_cast<uint64_t>(sw) << 32) | (static_cast<uint64_t>(l2) << 16) | oob);
+  if (t_encode_cache.find(k, m)) return CUDA_SUCCESS;
+  const CUresult r = g_encode_im2col(m, dt, rank, ptr, dims, strides, lo, hi, ch, px, es, il, sw, l2, oob);
+  if (r == CUDA_SUCCESS) t_encode_cache.put(k, *m);
+  return r;
+}
 
 const Driver* driver() {
   static Driver d;
@@ -76,15 +151,50 @@ const Driver* driver() {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
-            cudaSuccess && q == cudaDriverEntryPointSuccess)
-      d.tiled = reinterpret_cast<EncodeTiledFn>(fn);
+            cudaSuccess && q == cudaDriverEntryPointSuccess) {
+      g_encode_tiled = reinterpret_cast<EncodeTiledFn>(fn);
+      d.tiled = encode_tiled_cached;
+    }
     fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &fn, cudaEnableDefault, &q) ==
-            cudaSuccess && q == cudaDriverEntryPointSuccess)
-      d.im2col = reinterpret_cast<EncodeIm2colFn>(fn);
+            cudaSuccess && q == cudaDriverEntryPointSuccess) {
+      g_encode_im2col = reinterpret_cast<EncodeIm2colFn>(fn);
+      d.im2col = encode_im2col_cached;
+    }
     cudaDriverGetVersion(&d.version);
   });
   return &d;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size: a
+// driver call per launch otherwise (host-side planning cost of every call).
+cudaError_t ensure_smem_ptr(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::vector<std::pair<const void*, size_t>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const void* key = reinterpret_cast<const char*>(func) + dev;  // per device
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : done)
+      if (e.first == key && e.second >= bytes) return cudaSuccess;
+  }
+  const cudaError_t r = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (r == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(mu);
+    for (auto& e : done)
+      if (e.first == key) {
+        e.second = std::max(e.second, bytes);
+        return r;
+      }
+    done.emplace_back(key, bytes);
+  }
+  return r;
+}
+
+template <typename Params>
+cudaError_t ensure_smem(void (*kernel)(Params), size_t bytes) {
+  return ensure_smem_ptr(reinterpret_cast<const void*>(kernel), bytes);
 }
 
 struct DeviceInfo {
@@ -337,8 +447,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     if (p.total_tiles > di.sms || p.total_tiles % p.ksplit || ring < static_cast<size_t>(tb::kBM) * (BN + 4) * 4)
       return set_err(TIR_B200_ERR_UNSUPPORTED, "split-K plan does not fit (tiles %d, ksplit %d)", p.total_tiles,
                      p.ksplit);
-    CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(smem)));
+    CUDA_TRY(ensure_smem(tb::igemm_tc_kernel<BN, KS, EPI8>, smem));
     p.mc = 0;
     p.trace = g_trace;
     CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8>, p.total_tiles, p.ksplit, Cfg::kThreadsN, smem,
@@ -348,8 +457,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   }
   if constexpr (GP) {
     if (p.ksplit != 1) return kNotEligible;
-    CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8, false, true>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    CUDA_TRY(ensure_smem(tb::igemm_tc_kernel<BN, KS, EPI8, false, true>, smem));
     if (const int e = tb::options().max_ctas) grid = std::max(1, std::min(grid, e));
     p.mc = 0;
     p.trace = g_trace;
@@ -357,8 +465,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
     ++g_launches;
     return TIR_B200_OK;
   } else {
-  CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(smem)));
+  CUDA_TRY(ensure_smem(tb::igemm_tc_kernel<BN, KS, EPI8>, smem));
   // B-multicast CTA pairs (igemm.cuh mc_tile) for plain GEMMs with wide N tiles.
   p.mc = 0;
   if (use_pairs(p, BN) && grid >= 2) {
@@ -394,8 +501,7 @@ int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   p.trace = g_trace;
   if (p.mc == 2) {
     if constexpr (BN >= 128) {
-      CUDA_TRY(cudaFuncSetAttribute(tb::igemm_tc_kernel<BN, KS, EPI8, true>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+      CUDA_TRY(ensure_smem(tb::igemm_tc_kernel<BN, KS, EPI8, true>, smem));
       CUDA_TRY(launch_pdl_cluster(tb::igemm_tc_kernel<BN, KS, EPI8, true>, grid, 2, Cfg::kThreadsN, smem, stream,
                                   p));
     }
@@ -849,8 +955,7 @@ int launch_halo_bn(tb::HaloParams& p, cudaStream_t stream) {
   if (stages < 2) return kNotEligible;
   p.stages = stages;
   const size_t smem = Cfg::smem_bytes(p.stages, p.slab_rows, p.b_rows, p.stage_bytes);
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_halo_kernel<BN, KH, KW>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CUDA_TRY(ensure_smem(tb::conv_halo_kernel<BN, KH, KW>, smem));
   int grid = std::min(p.total_tiles, di.sms / keys * keys);
   if (const int e = tb::options().max_ctas) grid = std::max(1, std::min(grid, e));
   p.trace = g_trace;
@@ -993,8 +1098,7 @@ int conv_halo_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const flo
 
 template <int BN, int KH, int KW, int CI, int DW, bool D3>
 int launch_rowpack_k(tb::RowpackParams& p, size_t smem, cudaStream_t stream) {
-  CUDA_TRY(cudaFuncSetAttribute(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW, D3>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CUDA_TRY(ensure_smem(tb::conv_rowpack_kernel<BN, KH, KW, CI, DW, D3>, smem));
   const DeviceInfo di = device_info();
   const int grid = std::min(p.total_units, di.sms);
   p.trace = g_trace;
@@ -1527,7 +1631,7 @@ int launch_dep_tile(const Geo& g, const uint16_t* X, const uint16_t* W, const fl
   // The epilogue is a template flag so the plain kernel keeps its register budget.
   auto kern = epi.on() ? tb::dep_tile_kernel<K, S, R, T, TR, TC, true>
                        : tb::dep_tile_kernel<K, S, R, T, TR, TC, false>;
-  CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+  CUDA_TRY(ensure_smem(kern, smem));
   int per_sm = 0;
   CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
   const DeviceInfo di = device_info();
@@ -1623,11 +1727,13 @@ int conv_impl(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t*
 
 // ------------------------------------------------------------------ host-buffer paths
 
+constexpr int kHostMaxChunks = 16;
+
 struct HostCache {
   int dev = -1;
   cudaStream_t stream = nullptr;
-  cudaStream_t side[2] = {nullptr, nullptr};  // batch-chunk pipeline streams
-  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  cudaStream_t side[3] = {nullptr, nullptr, nullptr};  // batch-chunk pipeline: H2D, conv, D2H streams
+  cudaEvent_t ev[2 * kHostMaxChunks + 1] = {};          // weights / per-chunk H2D done / conv done
   void* dbuf = nullptr;
   size_t dbytes = 0;
   int* dflag = nullptr;
@@ -1784,35 +1890,39 @@ int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const 
   cudaStream_t st = t_host.stream;
   CUDA_TRY(cudaMemcpyAsync(d + xa, W, we * 2, cudaMemcpyHostToDevice, st));
   // Batch-chunk pipeline: images are independent (every output keeps its own
-  // reduction order, so a batch slice is bit-identical), so chunk c's H2D, conv
-  // and D2H are queued on one of three streams and the two PCIe directions and
-  // the GPU overlap across chunks. Only for convs that need no shared library
-  // workspace (CI / G a multiple of 8: no relayout kernels).
+  // reduction order, so a batch slice is bit-identical), so the chunks' H2D, conv
+  // and D2H overlap. Only for convs that need no shared library workspace
+  // (CI / G a multiple of 8: no relayout kernels).
   const int64_t cig = g.ci / g.g;
   const int nch = (cig % 8 == 0 && g.n >= 2 && tb::options().host_pipeline)
-                      ? static_cast<int>(std::min<int64_t>(g.n, 8)) : 1;
+                      ? static_cast<int>(std::min<int64_t>(g.n, tb::options().host_chunks)) : 1;
   const int64_t x_img = xe / g.n, y_img = ye / g.n;
+  const int nchunks = std::min(nch, kHostMaxChunks);
+  // Three streams: the H2D copies back to back on one, the convs on another, the
+  // D2H copies on a third (each waiting on its chunk's event), so the two copy
+  // directions and the GPU overlap across chunks without a chunk's D2H delaying
+  // a later chunk's H2D on a shared stream.
+  cudaStream_t sh = t_host.side[0], sc = t_host.side[1], sd = t_host.side[2];
   CUDA_TRY(cudaEventRecord(t_host.ev[0], st));  // weights uploaded
-  cudaStream_t streams[3] = {st, t_host.side[0], t_host.side[1]};
-  for (int c = 1; c < 3 && c < nch; ++c) CUDA_TRY(cudaStreamWaitEvent(streams[c], t_host.ev[0], 0));
-  for (int c = 0; c < nch; ++c) {
-    const int64_t n0 = g.n * c / nch, n1 = g.n * (c + 1) / nch;
-    cudaStream_t sc = streams[c % 3];
+  CUDA_TRY(cudaStreamWaitEvent(sc, t_host.ev[0], 0));
+  CUDA_TRY(cudaStreamWaitEvent(sh, t_host.ev[0], 0));  // buffers free of the previous call's work on st
+  for (int c = 0; c < nchunks; ++c) {
+    const int64_t n0 = g.n * c / nchunks, n1 = g.n * (c + 1) / nchunks;
     uint16_t* dx = reinterpret_cast<uint16_t*>(d) + n0 * x_img;
     float* dy = reinterpret_cast<float*>(d + xa + wa) + n0 * y_img;
-    CUDA_TRY(cudaMemcpyAsync(dx, X + n0 * x_img, (n1 - n0) * x_img * 2, cudaMemcpyHostToDevice, sc));
-    if (accumulate) CUDA_TRY(cudaMemcpyAsync(dy, Y + n0 * y_img, (n1 - n0) * y_img * 4, cudaMemcpyHostToDevice, sc));
+    CUDA_TRY(cudaMemcpyAsync(dx, X + n0 * x_img, (n1 - n0) * x_img * 2, cudaMemcpyHostToDevice, sh));
+    if (accumulate) CUDA_TRY(cudaMemcpyAsync(dy, Y + n0 * y_img, (n1 - n0) * y_img * 4, cudaMemcpyHostToDevice, sh));
+    CUDA_TRY(cudaEventRecord(t_host.ev[1 + c], sh));
+    CUDA_TRY(cudaStreamWaitEvent(sc, t_host.ev[1 + c], 0));
     tir_b200_conv_desc dc = *desc;
     dc.n = n1 - n0;
     rc = conv_impl(&dc, dx, reinterpret_cast<uint16_t*>(d + xa), dy, dy, accumulate, 0, Epi{}, sc);
     if (rc) return rc;
-    CUDA_TRY(cudaMemcpyAsync(Y + n0 * y_img, dy, (n1 - n0) * y_img * 4, cudaMemcpyDeviceToHost, sc));
+    CUDA_TRY(cudaEventRecord(t_host.ev[1 + kHostMaxChunks + c], sc));
+    CUDA_TRY(cudaStreamWaitEvent(sd, t_host.ev[1 + kHostMaxChunks + c], 0));
+    CUDA_TRY(cudaMemcpyAsync(Y + n0 * y_img, dy, (n1 - n0) * y_img * 4, cudaMemcpyDeviceToHost, sd));
   }
-  for (int c = 1; c < 3 && c < nch; ++c) {
-    CUDA_TRY(cudaEventRecord(t_host.ev[c], streams[c]));
-    CUDA_TRY(cudaStreamWaitEvent(st, t_host.ev[c], 0));
-  }
-  CUDA_TRY(cudaStreamSynchronize(st));
+  CUDA_TRY(cudaStreamSynchronize(sd));
   return TIR_B200_OK;
 }
 
