@@ -69,6 +69,14 @@ SMALL = {
     "DIL_ci64": tb.Conv("DIL", n=2, in_dhw=(1, 14, 14), ci=64, co=64, k=(1, 3, 3), p=(0, 2, 2), d=(1, 2, 2)),
     "GRP": tb.Conv("GRP", n=2, in_dhw=(1, 12, 12), ci=64, co=128, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), groups=4),
     "GRP_g2": tb.Conv("GRP", n=1, in_dhw=(1, 10, 10), ci=128, co=128, k=(1, 3, 3), p=(0, 1, 1), groups=2),
+    # group-packed igemm (GP): 4 groups of 16 channels per 64-channel piece, two piece blocks (G = 8)
+    "GRP_gp16": tb.Conv("GRP", n=2, in_dhw=(1, 13, 11), ci=128, co=256, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
+                        groups=8),
+    # GP with 2 groups of 32 channels per piece (BN = 64), a 1x7 window (taps * cig <= 256)
+    "GRP_gp32": tb.Conv("GRP", n=1, in_dhw=(1, 9, 12), ci=64, co=64, k=(1, 1, 7), p=(0, 0, 3), groups=2),
+    # rowpack: an image narrower than one 16-column tile (Wt = OW) and a 3-D shape with depth stride 1
+    "C2D_stem7_narrow": tb.Conv("C2D", n=3, in_dhw=(1, 20, 16), ci=3, co=64, k=(1, 7, 7), s=(1, 2, 2), p=(0, 3, 3)),
+    "C3D_rp_s1d": tb.Conv("C3D", n=1, in_dhw=(5, 16, 16), ci=3, co=32, k=(3, 3, 3), s=(1, 2, 2), p=(1, 1, 1)),
     "T2D": tb.Conv("T2D", n=2, in_dhw=(1, 4, 4), ci=64, co=64, k=(1, 4, 4), s=(1, 2, 2), p=(0, 1, 1), transposed=True),
     "T2D_k3": tb.Conv("T2D", n=1, in_dhw=(1, 5, 6), ci=64, co=32, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1), transposed=True),
     "DEP": tb.Conv("DEP", n=2, in_dhw=(1, 9, 9), ci=32, co=32, k=(1, 3, 3), p=(0, 1, 1), groups=32),
@@ -112,7 +120,8 @@ def test_conv_d2_within_tolerance(name, cuda):
         assert O.tensors_bitwise_equal(got, want)
 
 
-@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D", "C3D_rp", "C2D_stem3", "DIL_rp"])
+@pytest.mark.parametrize("name", ["C2D", "GRP", "T2D", "DEP", "C1D", "C3D_rp", "C2D_stem3", "DIL_rp", "GRP_gp16",
+                                  "GRP_gp32"])
 def test_conv_accumulate_and_fp16_out(name, cuda):
     import torch
 
@@ -345,7 +354,8 @@ def kernels_launched(fn):
     return [e.name for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
 
 
-@pytest.mark.parametrize("name", ["C3D_rp", "C3D_rp_odd", "C2D_stem7", "C2D_stem3", "DIL_rp"])
+@pytest.mark.parametrize("name", ["C3D_rp", "C3D_rp_odd", "C2D_stem7", "C2D_stem3", "DIL_rp", "C2D_stem7_narrow",
+                                  "C3D_rp_s1d"])
 def test_rowpack_vs_im2col_exact(name, option, cuda):
     """The rowpack kernel (default for these shapes: A operand packed in TMEM) and the
     (kw, c) relayout + im2col path (no_rowpack = 1) both equal the oracle bit for bit."""
@@ -362,6 +372,25 @@ def test_rowpack_vs_im2col_exact(name, option, cuda):
     names = kernels_launched(lambda: out.setdefault("y", run_conv(spec, x, w, cuda)))
     assert not any("conv_rowpack_kernel" in k for k in names), names
     assert O.tensors_bitwise_equal(out["y"], want)
+
+
+@pytest.mark.parametrize("name", ["GRP", "GRP_gp16", "GRP_gp32"])
+def test_group_packed_vs_per_group_exact(name, option, cuda):
+    """The group-packed igemm (default for 16 / 32 channels per group, 32 per output
+    group) and the per-group narrow-piece plan (no_gpack = 1) both equal the oracle
+    bit for bit; the packed plan launches the GP instantiation."""
+    spec = SMALL[name]
+    x = O.reference_tensor(spec.x_shape(), 35)
+    w = O.reference_tensor(spec.w_shape(), 36)
+    want = O.conv(ospec(spec), x, w, threads=8)
+    out = {}
+    names = kernels_launched(lambda: out.setdefault("y", run_conv(spec, x, w, cuda)))
+    assert any("igemm_tc_kernel" in k and k.rstrip(">)").count("true") for k in names), names
+    assert O.tensors_bitwise_equal(out["y"], want)
+    option("no_gpack", 1)
+    out = {}
+    run = run_conv(spec, x, w, cuda)
+    assert O.tensors_bitwise_equal(run, want)
 
 
 @pytest.mark.parametrize("name", ["DIL", "C3D"])

@@ -1,2 +1,1 @@
-for c in 4 8 16; do TIR_B200_HOST_CHUNKS=$c timeout 300 python bench.py --op C2D --no-ops --no-cpu --no-nets --steps 50 --warmup 5 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print('chunks $c e2e', d['e2e']['value'], d['e2e']['ms_per_step'])"; done
-timeout 600 python -m pytest tests -m gpu -x -q -k "host or dropin or ref_format" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_epilogue.py -m gpu -x -q -k "gp16 or gp32 or group_packed or narrow or s1d or GRP" 2>&1 | tail -15
