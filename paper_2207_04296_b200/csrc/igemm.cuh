@@ -122,6 +122,7 @@ struct alignas(64) IgemmParams {
                         // boxes {64 K, BN rows} (attention's Q K^T reads K straight from QKV)
   int32_t mc;           // 2: cta_group::2 CTA pair (CG2 instantiation, clusters of 2): see mc_tile
   int32_t batch_z2;     // problems per z1
+  int32_t l2_prefetch;  // producers prefetch their share of the first stage's A into L2 before the PDL wait
   int32_t gp_taps, gp_kpg;  // GP instantiation (group-packed): taps, K16 steps per packed group (cig / 16)
   BatchAxis ba, bb, bc; // A / B / C coordinates per problem
 };
@@ -583,6 +584,27 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     };
     ProdTile pt{};
     if (static_cast<int>(blockIdx.x) < p.total_tiles) pt = prod_setup(blockIdx.x);
+    // Optional: this producer's share of the first stage -> L2 before the wait (a
+    // prefetch only moves DRAM latency under the preceding grid's tail; the real
+    // loads still come after the wait, and L2 is the point of coherence).
+    if (p.l2_prefetch && !cg2 && static_cast<int>(blockIdx.x) < p.total_tiles && elect_one()) {
+      const int pc0 = pt.st0 * pps;
+      for (int j = pw; j < pps; j += kProducers) {
+        const int pc = pc0 + j;
+        if (a_mode == A_TILED) {
+          tma_prefetch_2d(pt.tmA, pc * kBK + pt.a_c, pt.m0 + pt.a_r);
+          continue;
+        }
+        if (pc >= pt.npieces) break;
+        const int4 e = pt.ptab[pc];
+        const int c = pt.cbase + e.x;
+        const uint16_t ox = static_cast<uint16_t>(e.y & 0xFFFF), oy = static_cast<uint16_t>(e.y >> 16);
+        if (a_mode == A_IM2COL4) tma_prefetch_im2col_4d(pt.tmA, c, pt.cx, pt.cy, pt.n, ox, oy);
+        else if (a_mode == A_IM2COL3) tma_prefetch_im2col_3d(pt.tmA, c, pt.cx, pt.n, ox);
+        else tma_prefetch_im2col_5d(pt.tmA, c, pt.cx, pt.cy, pt.cz, pt.n, ox, oy, static_cast<uint16_t>(e.z));
+      }
+    }
+    __syncwarp();
     // Everything above is parameter arithmetic: it runs before the wait, so
     // the first TMA issues right after the preceding grid's memory is visible.
     pdl_wait();  // operands may be produced by the preceding kernel

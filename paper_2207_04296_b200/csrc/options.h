@@ -26,6 +26,7 @@ struct Options {
   int bn = 0;              // > 0: force the igemm N tile
   int ksplit = 0;          // > 0: force the split-K factor (cluster-reduced, deterministic)
   int no_halo = 0;         // 1: stride-1 convs take the im2col kernel
+  int igemm_prefetch = 0;  // 1: im2col producers prefetch the first stage's A into L2 before the PDL wait
   int no_gpack = 0;        // 1: grouped convs with 16 / 32 channels per group take one narrow im2col piece per group
   int no_rowpack = 0;      // 1: CI = 3 stems / C3D take the (kw, c) relayout + im2col kernel
   int rp_backoff = 64;     // rowpack: ns between barrier polls of producers / epilogue (0: spin)
@@ -57,7 +58,8 @@ inline const OptionEntry* option_table(int* count) {
       {"ks", &Options::ks},                 {"ks_strict", &Options::ks_strict},
       {"no_tma_store", &Options::no_tma_store}, {"bn", &Options::bn},
       {"ksplit", &Options::ksplit},         {"no_halo", &Options::no_halo},
-      {"no_rowpack", &Options::no_rowpack},     {"no_gpack", &Options::no_gpack},     {"rowpack_debug", &Options::rowpack_debug},
+      {"no_rowpack", &Options::no_rowpack},     {"no_gpack", &Options::no_gpack},
+      {"igemm_prefetch", &Options::igemm_prefetch},     {"rowpack_debug", &Options::rowpack_debug},
       {"rp_backoff", &Options::rp_backoff},     {"rp_backoff2", &Options::rp_backoff2},
       {"pack_hw", &Options::pack_hw},       {"pack_kw", &Options::pack_kw},
       {"pack_gather", &Options::pack_gather}, {"dep_simple", &Options::dep_simple},

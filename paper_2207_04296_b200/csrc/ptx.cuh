@@ -228,6 +228,26 @@ __device__ __forceinline__ void named_bar_sync(uint32_t id, uint32_t count) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
+// L2 prefetches of im2col boxes (same coordinates / offsets as the loads below).
+__device__ __forceinline__ void tma_prefetch_im2col_3d(const CUtensorMap* m, int c, int w, int n, uint16_t ow) {
+  asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.im2col [%0, {%1, %2, %3}], {%4};" ::"l"(m), "r"(c),
+               "r"(w), "r"(n), "h"(ow)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_im2col_4d(const CUtensorMap* m, int c, int w, int h, int n,
+                                                       uint16_t ow, uint16_t oh) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.im2col [%0, {%1, %2, %3, %4}], {%5, %6};" ::"l"(m),
+               "r"(c), "r"(w), "r"(h), "r"(n), "h"(ow), "h"(oh)
+               : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_im2col_5d(const CUtensorMap* m, int c, int w, int h, int d, int n,
+                                                       uint16_t ow, uint16_t oh, uint16_t od) {
+  asm volatile("cp.async.bulk.prefetch.tensor.5d.L2.global.im2col [%0, {%1, %2, %3, %4, %5}], {%6, %7, %8};" ::"l"(
+                   m),
+               "r"(c), "r"(w), "r"(h), "r"(d), "r"(n), "h"(ow), "h"(oh), "h"(od)
+               : "memory");
+}
+
 // im2col loads: coordinates (c, w[, h[, d]], n), offsets (w[, h[, d]]).
 __device__ __forceinline__ void tma_im2col_3d(void* dst, const CUtensorMap* m, uint64_t* bar, int c,
                                               int w, int n, uint16_t ow) {

@@ -400,6 +400,7 @@ template <int BN, int KS, bool EPI8, bool GP = false>
 int launch_igemm_bn(tb::IgemmParams& p, cudaStream_t stream) {
   using Cfg = tb::IgemmCfg<BN, KS, EPI8, GP>;
   const DeviceInfo di = device_info();
+  p.l2_prefetch = tb::options().igemm_prefetch;
   const int table = p.total_pieces * 16;
   // Stage the bias in shared memory for the TMA-store epilogue when it is small
   // and every 32-column chunk starts 16-byte aligned inside it.
