@@ -38,6 +38,7 @@ constexpr int kRpThreads = 544;  // warps 0-3 epilogue, 4-11 builders, 12 MMA, 1
 constexpr int kRpMmaWarp = 12;   // on SM sub-partition 0 (warp % 4 == 0)
 constexpr int kRpMaxSlots = 5;   // TMEM accumulator ring (p.nacc slots): output depths in flight + one draining
 constexpr int kRpMaxA = 4;       // TMEM A-buffer ring (p.nabuf buffers of KWORDS columns after the accumulators)
+constexpr int kRpDescRing = 16;  // plane descriptors in flight (> raw stages + A buffers: no reuse race)
 
 struct alignas(64) RowpackParams {
   CUtensorMap tmX;  // 3-D over X[N*D, H, W*CI] fp16: box {box_w, box_h, 1}, no swizzle
@@ -57,7 +58,7 @@ struct alignas(64) RowpackParams {
   int32_t act;        // 0 none, 1 ReLU, 2 ReLU6, 3 GELU (epi_act)
   int32_t backoff_ns, backoff_ns2;  // poll back-off of producers / epilogue, and of the builders
   int32_t debug;  // timing experiments only (wrong results): 1 builders skip the raw loads, 2 no output
-                  // stores, 4 no A build at all
+                  // stores, 4 no A build at all, 16 no raw loads
   unsigned long long* trace;
 };
 
@@ -246,6 +247,9 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
   uint64_t* tempty = tfull + kRpMaxSlots;  // [kRpMaxSlots]
   uint64_t* bfull = tempty + kRpMaxSlots;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 1);
+  // per-plane MMA descriptors (kRpDescRing x 3 uint4), written by the producer that
+  // loads the plane, read by the MMA thread after the plane's A buffer is published
+  uint4* pdesc = reinterpret_cast<uint4*>((reinterpret_cast<uintptr_t>(tmem_slot + 1) + 15) & ~uintptr_t(15));
 
   if (threadIdx.x == 0) trace_event(p.trace, TR_ENTRY);
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -322,7 +326,9 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
         }
       }
       int it = 0;
-      for (int u = blockIdx.x; u < p.total_units; u += gridDim.x) {
+      int ubase_p = 0;
+      const uint32_t kd_step_p = (static_cast<uint32_t>(p.kp) * Cfg::kBRowBytes) >> 4;
+      for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ubase_p += p.od) {
         int n, th, tw;
         decompose(u, n, th, tw);
         // the box starts `shift` elements before the tile's first input element (16-byte aligned)
@@ -336,9 +342,31 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
             const uint32_t slot = static_cast<uint32_t>(it % S), phase = static_cast<uint32_t>(it / S) & 1u;
             mbar_wait_backoff(&rempty[slot], phase ^ 1, p.backoff_ns);
             if (trace && it < 128) trace[2 * it] = clock64();
-            mbar_arrive_expect_tx(&rfull[slot], static_cast<uint32_t>(p.box_w * p.box_h * 2));
-            tma_load_3d(raw + static_cast<size_t>(slot) * p.slot_bytes, &p.tmX, &rfull[slot], x0, y0,
-                        n * p.d + di);
+            // the plane's MMA bookkeeping, off the MMA thread (released by the rfull arrive
+            // below; the MMA thread reads it after acquiring the plane's afull); 2-D convs
+            // have one plane per tile, which the MMA thread handles inline
+            if constexpr (D3) {
+              uint32_t w[12] = {static_cast<uint32_t>(o1 - o0 + 1), 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+              for (int i = 0; i < kRpMaxSlots - 1 && o0 + i <= o1; ++i) {
+                const int od = o0 + i, g = ubase_p + od, base = od * p.sd - p.pd;
+                const uint32_t first = di == (base > 0 ? base : 0);
+                const uint32_t last = di == (base + p.kd - 1 < p.d - 1 ? base + p.kd - 1 : p.d - 1);
+                w[1 + 2 * i] = static_cast<uint32_t>(di - base) * kd_step_p;
+                w[2 + 2 * i] = static_cast<uint32_t>(g % nacc) | (first << 4) | (last << 5) |
+                               ((static_cast<uint32_t>(g / nacc) & 1u) << 6);
+              }
+              uint4* dst = pdesc + (it % kRpDescRing) * 3;
+              dst[0] = make_uint4(w[0], w[1], w[2], w[3]);
+              dst[1] = make_uint4(w[4], w[5], w[6], w[7]);
+              dst[2] = make_uint4(w[8], w[9], w[10], w[11]);
+            }
+            if (p.debug & 16) {
+              mbar_arrive(&rfull[slot]);  // timing experiment: no raw load
+            } else {
+              mbar_arrive_expect_tx(&rfull[slot], static_cast<uint32_t>(p.box_w * p.box_h * 2));
+              tma_load_3d(raw + static_cast<size_t>(slot) * p.slot_bytes, &p.tmX, &rfull[slot], x0, y0,
+                          n * p.d + di);
+            }
             if (trace && it < 128) trace[2 * it + 1] = clock64();
           }
           ++it;
@@ -414,20 +442,31 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
     // drained by the epilogue while the MMAs carry on with the next planes.
     const uint64_t b0 = smem_desc(smem_u32(sB), b_rows * Cfg::kBRowBytes, 8 * Cfg::kBRowBytes, Cfg::kBLayout);
     constexpr uint32_t kBk16 = (16 * Cfg::kBRowBytes) >> 4;  // one K16 step of B (descriptor units)
-    const uint32_t kd_step = (static_cast<uint32_t>(p.kp) * Cfg::kBRowBytes) >> 4;
     if (static_cast<int>(blockIdx.x) < p.total_units) {
       mbar_wait(bfull, 0);
       tc_fence_after();
     }
-    uint32_t pi = 0;
-    int ubase = 0;  // sequence number of the unit's output depth 0
+    // the CTA's planes in order (the producers and builders walk the same sequence)
+    int per_unit = 0;
+    for (int di = plane_lo; di <= plane_hi; ++di) {
+      int o0, o1;
+      od_range(di, o0, o1);
+      per_unit += o0 <= o1;
+    }
+    const int my_units = static_cast<int>(blockIdx.x) < p.total_units
+                             ? (p.total_units - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1
+                             : 0;
+    const uint32_t nplanes = static_cast<uint32_t>(my_units * per_unit);
     bool first_unit = true;
-    for (int u = blockIdx.x; u < p.total_units; u += gridDim.x, ubase += p.od) {
-      for (int di = plane_lo; di <= plane_hi; ++di) {
-        int o0, o1;
-        od_range(di, o0, o1);
-        if (o0 > o1) continue;
+    {
+      for (uint32_t pi = 0; pi < nplanes; ++pi) {
         const uint32_t ab = pi % nabuf, use = pi / nabuf;
+        // The tensor pipe takes the next MMA only about when the previous one starts,
+        // so anything the issuing thread does between MMAs is a pipe bubble (measured:
+        // ~100 cycles per depth and ~450 per plane of bookkeeping halved the MMA rate).
+        // Everything of the plane — each depth's accumulator slot, B offset, first /
+        // last flags, the slot waits — is settled before the first MMA; the issue is
+        // then straight-line MMAs and commits.
         mbar_wait(&afull[ab], use & 1);
         tc_fence_after();
         if (trace && lane == 0 && pi < 128) trace[256 + 2 * pi] = clock64();
@@ -435,33 +474,46 @@ __global__ void __launch_bounds__(kRpThreads, 1) conv_rowpack_kernel(const __gri
           trace_event(p.trace, TR_FIRST_FULL);
           first_unit = false;
         }
+        // the plane's depths, B offsets, accumulator slots and first / last flags were
+        // computed by its producer: straight-line MMAs from here (the tensor pipe takes
+        // the next MMA only about when the previous one starts, so bookkeeping between
+        // MMAs is a bubble: ~800 cycles per plane when the MMA thread did it itself)
+        uint32_t w[12];
+        if constexpr (D3) {
+          const uint4* dsc = pdesc + (pi % kRpDescRing) * 3;
+          const uint4 q0 = dsc[0], q1 = dsc[1], q2 = dsc[2];
+          w[0] = q0.x, w[1] = q0.y, w[2] = q0.z, w[3] = q0.w, w[4] = q1.x, w[5] = q1.y;
+          w[6] = q1.z, w[7] = q1.w, w[8] = q2.x, w[9] = q2.y, w[10] = q2.z, w[11] = q2.w;
+        } else {  // one plane per tile: depth 0, kd 0, the tile's own ring slot
+          w[0] = 1;
+          w[1] = 0;
+          w[2] = (pi % nacc) | (1u << 4) | (1u << 5) | (((pi / nacc) & 1u) << 6);
+        }
+        const int nod = static_cast<int>(w[0]);
         const uint32_t a = tmem_base + a_col + ab * kWords;
-        // one elected thread issues the whole plane (no per-depth warp reconvergence)
         if (elect_one()) {
-          for (int od = o0; od <= o1; ++od) {
-            const int g = ubase + od;
-            const uint32_t sl = static_cast<uint32_t>(g % nacc), sph = static_cast<uint32_t>(g / nacc) & 1u;
-            const int base = od * p.sd - p.pd;  // input plane of kd = 0
-            const int kd = di - base;
-            const bool first = di == (base > 0 ? base : 0);  // depth od's planes are contiguous
-            const bool last = di == (base + p.kd - 1 < p.d - 1 ? base + p.kd - 1 : p.d - 1);
-            if (first) {
-              mbar_wait(&tempty[sl], sph ^ 1);
-              tc_fence_after();
-            }
-            const uint32_t d = tmem_base + sl * BN;
-            const uint64_t bk = b0 + static_cast<uint32_t>(kd) * kd_step;
+          constexpr int kMaxOd = kRpMaxSlots - 1;
 #pragma unroll
-            for (int st = 0; st < kSteps; ++st)
-              umma_f16_ts(d, a + 8 * st, bk + st * kBk16, Cfg::kIdesc, (first && st == 0) ? 0u : 1u);
-            if (last) umma_commit(&tfull[sl]);
-            if (trace && pi < 48 && od - o0 < 4) trace[832 + 4 * pi + (od - o0)] = clock64();
+          for (int i = 0; i < kMaxOd; ++i) {
+            if (i < nod) {
+              const uint32_t fl = w[2 + 2 * i], sl = fl & 15u;
+              const bool fst = (fl >> 4) & 1u, lst = (fl >> 5) & 1u;
+              if (fst) {
+                mbar_wait(&tempty[sl], ((fl >> 6) & 1u) ^ 1u);  // the slot's previous depth was drained
+                tc_fence_after();
+              }
+              const uint32_t d = tmem_base + sl * BN;
+              const uint64_t bk = b0 + w[1 + 2 * i];
+#pragma unroll
+              for (int st = 0; st < kSteps; ++st)
+                umma_f16_ts(d, a + 8 * st, bk + st * kBk16, Cfg::kIdesc, (fst && st == 0) ? 0u : 1u);
+              if (lst) umma_commit(&tfull[sl]);
+            }
           }
           umma_commit(&afree[ab]);
         }
         __syncwarp();
         if (trace && lane == 0 && pi < 128) trace[257 + 2 * pi] = clock64();
-        ++pi;
       }
     }
   } else if (warp < 4) {

@@ -1169,7 +1169,7 @@ int conv_rowpack_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const 
   const int64_t b_bytes = g.k[0] * kp * bn * 2;
   const int stage_bytes = static_cast<int>((R * Wt * 32 * (out_f16 ? 2 : 4) + 1023) / 1024 * 1024);
   const int slot_bytes = static_cast<int>((box_w * box_h * 2 + 1023) / 1024 * 1024);
-  const int64_t fixed = 1024 + b_bytes + 2 * stage_bytes + 256;
+  const int64_t fixed = 1024 + b_bytes + 2 * stage_bytes + 256 + 16 * 3 * 16 + 16;  // + plane-descriptor ring
   // deep raw ring: each plane's box is a latency-bound handful of short DRAM rows
   const int stages = static_cast<int>(std::min<int64_t>(8, (di.smem_optin - fixed) / slot_bytes));
   if (stages < 2) return kNotEligible;

@@ -47,7 +47,7 @@ def capture(op, launches=8):
     for b in bufs:
         ev = b[8192:8192 + 8 * 256].view(256, 8)[:, :8].cpu().tolist()
         cta = b[2048:2048 + 4 * 1024].view(1024, 4).cpu().tolist()
-        out.append((ev, cta, b[:1024].cpu().tolist()))
+        out.append((ev, cta, b[:2048].cpu().tolist()))
     return out
 
 
@@ -98,6 +98,9 @@ def main():
         bld = [tuple(clk[640 + 3 * i + j] - t0 for j in range(3)) for i in range(64) if clk[640 + 3 * i]]
         if bld:
             print("  builder warp (raw ok, A buffer free, A published):", bld[:16])
+        pre = [(clk[1024 + 4 * i] - t0, clk[1025 + 4 * i] - t0) for i in range(64) if clk[1024 + 4 * i]]
+        if pre:
+            print("  MMA plane preamble (start, before A wait) (rowpack):", pre[:12])
         ods = [[clk[832 + 4 * i + j] - t0 for j in range(4) if clk[832 + 4 * i + j]] for i in range(48)
                if clk[832 + 4 * i]]
         if ods:
