@@ -345,9 +345,12 @@ __global__ void __launch_bounds__(128, 3) dep_tile_kernel(const __grid_constant_
           u.w = *reinterpret_cast<uint32_t*>(&hh[3]);
           *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(p.Y) + off) = u;
         } else {
+          // one 32-byte store per thread (a whole sector; two 16-byte halves would each
+          // leave it half written per instruction)
           float* y = reinterpret_cast<float*>(p.Y) + off;
-          reinterpret_cast<float4*>(y)[0] = make_float4(f[0].x, f[0].y, f[1].x, f[1].y);
-          reinterpret_cast<float4*>(y)[1] = make_float4(f[2].x, f[2].y, f[3].x, f[3].y);
+          asm volatile("st.global.v8.f32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(y), "f"(f[0].x),
+                       "f"(f[0].y), "f"(f[1].x), "f"(f[1].y), "f"(f[2].x), "f"(f[2].y), "f"(f[3].x), "f"(f[3].y)
+                       : "memory");
         }
       }
   }

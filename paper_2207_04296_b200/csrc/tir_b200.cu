@@ -1648,7 +1648,9 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
     return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: 2-D (NHWC) depthwise only");
   if (epi.residual) return set_err(TIR_B200_ERR_UNSUPPORTED, "DEP: residual epilogue not supported");
   // Fast path: 3x3, stride 1 or 2, no dilation, 32-channel blocks, aligned operands.
-  const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) && (reinterpret_cast<uintptr_t>(Y) % 16 == 0) &&
+  // fp32 outputs are written as 32-byte vectors (dep.cuh st.global.v8)
+  const bool aligned = (reinterpret_cast<uintptr_t>(W) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(Y) % (out_f16 ? 16 : 32) == 0) &&
                        (!accumulate || reinterpret_cast<uintptr_t>(Yin) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(X) % 16 == 0);
   if (!tb::options().dep_simple && aligned && g.ci % 8 == 0 && g.ci >= 32 && g.k[1] == 3 && g.k[2] == 3 &&
