@@ -281,31 +281,21 @@ __device__ __forceinline__ float4 ld_cluster_f4(uint32_t addr) {
   return v;
 }
 
-// Deterministic split-K. The ksplit CTAs of a cluster (consecutive tile ids:
-// the split index is fastest) hold the fp32 partials of ONE output tile in
-// shared memory ([128][BN + 4], written by the epilogue warps). After a cluster
-// barrier, cluster rank r combines rows [r*R, (r+1)*R) of the tile over all
-// ranks through distributed shared memory in the fixed order
-// ((p_0 + p_1) + p_2) + ..., then applies the C-ABI epilogue — (Yin +) sum,
-// + bias, + residual, activation — and stores 16-byte vectors at the output
-// pixel of each row (row-linear or, for T2D classes, strided). No memset, no
-// atomics: the result is identical on every run. A second barrier keeps every
-// partial alive until all ranks have read it. All threads of the CTA take part.
+// Output element offset of each row this cluster rank combines (-1: past the
+// sub-problem), written to row_off[0, rows) by threads [0, nthr). The epilogue warps
+// call it while the MMAs run, so the combine finds its row offsets ready.
 template <int BN>
-__device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float* part, int64_t* row_off) {
-  mc_cluster_sync();  // every partial of the cluster is written (release / acquire)
+__device__ __forceinline__ void split_row_offsets(const IgemmParams& p, int64_t* row_off, int tid, int nthr) {
   uint32_t rank;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
-  const int ks = p.ksplit;
   const int tile = blockIdx.x;
-  const bool active = tile < p.total_tiles;
+  if (tile >= p.total_tiles) return;
   int s = 0, mt = 0, g = 0, nt = 0, kk = 0;
-  if (active) decompose_tile(p, tile, s, mt, g, nt, kk);
+  decompose_tile(p, tile, s, mt, g, nt, kk);
   const SubProb& sp = p.sub[s];
-  const int rows = (kBM + ks - 1) / ks;
+  const int rows = (kBM + p.ksplit - 1) / p.ksplit;
   const int r0 = static_cast<int>(rank) * rows, r1 = min(kBM, r0 + rows);
-  // output element offset of each of this rank's rows (-1: past the sub-problem)
-  for (int r = r0 + threadIdx.x; active && r < r1; r += blockDim.x) {
+  for (int r = r0 + tid; r < r1; r += nthr) {
     const int m = mt * kBM + r;
     int64_t off = -1;
     if (m < sp.m_count) {
@@ -320,90 +310,137 @@ __device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float
     }
     row_off[r - r0] = off;
   }
-  __syncthreads();
-  if (active) {
-    pdl_wait();  // Yin / residual may come from the preceding kernel
-    constexpr int kV = BN / 4;  // float4 per partial row
-    constexpr int kU = 2;       // items per thread and pass
-    constexpr int kMaxK = 8;    // every split's remote load of a pass is in flight at once
-    const uint32_t base = smem_u32(part);
-    const int valid = p.cog - nt * BN;
-    const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
-                        (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
-    const int items = (r1 - r0) * kV;
+}
+
+// One rank's share of the split-K combine: passes of KU items (float4 of the
+// partial rows [r0, r1)) per thread, every split's load of a pass in flight at
+// once; the cluster barrier is ARRIVED as soon as the last pass's remote loads
+// have been consumed (peers may then exit), and WAITED after the stores.
+template <int BN, int KMAX, int KU>
+__device__ __forceinline__ void cluster_combine(const IgemmParams& p, uint32_t base, const int64_t* row_off, int r0,
+                                                int r1, int g, int nt, bool active) {
+  constexpr int kV = BN / 4;  // float4 per partial row
+  const int ks = p.ksplit;
+  const int valid = p.cog - nt * BN;
+  const bool vec_ok = (p.ldy % 8 == 0) && (p.cog % 8 == 0) && ((reinterpret_cast<uintptr_t>(p.Y) & 15) == 0) &&
+                      (!p.accumulate || (reinterpret_cast<uintptr_t>(p.Yin) & 15) == 0);
+  const int items = active ? (r1 - r0) * kV : 0;
+  const int per_pass = KU * static_cast<int>(blockDim.x);
+  const int passes = (items + per_pass - 1) / per_pass;  // CTA-uniform
+  if (passes == 0) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (active) pdl_wait();  // Yin / residual may come from the preceding kernel
 #pragma unroll 1
-    for (int i0 = threadIdx.x; i0 < items; i0 += kU * blockDim.x) {
-      float4 t[kMaxK][kU];
+  for (int pass = 0; pass < passes; ++pass) {
+    const int i0 = pass * per_pass + static_cast<int>(threadIdx.x);
+    float4 t[KMAX][KU];
 #pragma unroll
-      for (int k = 0; k < kMaxK; ++k) {
-        if (k < ks) {
-          uint32_t rb;
-          asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(base), "r"(k));
+    for (int k = 0; k < KMAX; ++k) {
+      if (k < ks) {
+        uint32_t rb;
+        asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(rb) : "r"(base), "r"(k));
 #pragma unroll
-          for (int u = 0; u < kU; ++u) {
-            const int i = i0 + u * blockDim.x;
-            if (i < items) {
-              const int row = r0 + i / kV, col = (i % kV) * 4;
-              t[k][u] = ld_cluster_f4(rb + static_cast<uint32_t>((row * (BN + 4) + col) * 4));
-            }
+        for (int u = 0; u < KU; ++u) {
+          const int i = i0 + u * static_cast<int>(blockDim.x);
+          if (i < items) {
+            const int row = r0 + i / kV, col = (i % kV) * 4;
+            t[k][u] = ld_cluster_f4(rb + static_cast<uint32_t>((row * (BN + 4) + col) * 4));
           }
-        }
-      }
-      float4 v[kU];
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        v[u] = t[0][u];
-#pragma unroll
-        for (int k = 1; k < kMaxK; ++k) {  // fixed order ((p_0 + p_1) + p_2) + ...
-          if (k < ks) {
-            v[u].x = v[u].x + t[k][u].x; v[u].y = v[u].y + t[k][u].y;
-            v[u].z = v[u].z + t[k][u].z; v[u].w = v[u].w + t[k][u].w;
-          }
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < kU; ++u) {
-        const int i = i0 + u * blockDim.x;
-        if (i >= items) continue;
-        const int row = i / kV, col = (i % kV) * 4;
-        const int64_t ro = row_off[row];
-        if (ro < 0 || col >= valid) continue;
-        const int64_t off = ro + col;
-        const int lim = valid - col;
-        const bool vec = vec_ok && lim >= 4;
-        float* vv = reinterpret_cast<float*>(&v[u]);
-        if (p.accumulate) {
-          if (vec) {
-            const float4 y0 = *reinterpret_cast<const float4*>(p.Yin + off);
-            vv[0] = y0.x + vv[0]; vv[1] = y0.y + vv[1]; vv[2] = y0.z + vv[2]; vv[3] = y0.w + vv[3];
-          } else {
-            for (int j = 0; j < 4 && j < lim; ++j) vv[j] = p.Yin[off + j] + vv[j];
-          }
-        }
-        if (p.bias || p.relu || p.residual)
-          epi_run<4>(vv, p.bias, g * p.cog + nt * BN + col, lim, p.residual ? p.residual + off : nullptr, p.relu);
-        if (p.out_f16) {
-          __half* yp = reinterpret_cast<__half*>(p.Y) + off;
-          if (vec) {
-            __half2 h0 = __floats2half2_rn(vv[0], vv[1]), h1 = __floats2half2_rn(vv[2], vv[3]);
-            uint2 w2;
-            w2.x = *reinterpret_cast<uint32_t*>(&h0);
-            w2.y = *reinterpret_cast<uint32_t*>(&h1);
-            *reinterpret_cast<uint2*>(yp) = w2;
-          } else {
-            for (int j = 0; j < 4 && j < lim; ++j) yp[j] = __float2half_rn(vv[j]);
-          }
-        } else {
-          float* yp = reinterpret_cast<float*>(p.Y) + off;
-          if (vec) *reinterpret_cast<float4*>(yp) = v[u];
-          else
-            for (int j = 0; j < 4 && j < lim; ++j) yp[j] = vv[j];
         }
       }
     }
+    float4 v[KU];
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      v[u] = t[0][u];
+#pragma unroll
+      for (int k = 1; k < KMAX; ++k) {  // fixed order ((p_0 + p_1) + p_2) + ...
+        if (k < ks) {
+          v[u].x = v[u].x + t[k][u].x; v[u].y = v[u].y + t[k][u].y;
+          v[u].z = v[u].z + t[k][u].z; v[u].w = v[u].w + t[k][u].w;
+        }
+      }
+    }
+    if (pass == passes - 1) {  // every remote read of this CTA is done (the sums consumed them)
+      if (threadIdx.x == 0) trace_x(p.trace, 7);
+      asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+    }
+#pragma unroll
+    for (int u = 0; u < KU; ++u) {
+      const int i = i0 + u * static_cast<int>(blockDim.x);
+      if (i >= items) continue;
+      const int row = i / kV, col = (i % kV) * 4;
+      const int64_t ro = row_off[row];
+      if (ro < 0 || col >= valid) continue;
+      const int64_t off = ro + col;
+      const int lim = valid - col;
+      const bool vec = vec_ok && lim >= 4;
+      float* vv = reinterpret_cast<float*>(&v[u]);
+      if (p.accumulate) {
+        if (vec) {
+          const float4 y0 = *reinterpret_cast<const float4*>(p.Yin + off);
+          vv[0] = y0.x + vv[0]; vv[1] = y0.y + vv[1]; vv[2] = y0.z + vv[2]; vv[3] = y0.w + vv[3];
+        } else {
+          for (int j = 0; j < 4 && j < lim; ++j) vv[j] = p.Yin[off + j] + vv[j];
+        }
+      }
+      if (p.bias || p.relu || p.residual)
+        epi_run<4>(vv, p.bias, g * p.cog + nt * BN + col, lim, p.residual ? p.residual + off : nullptr, p.relu);
+      if (p.out_f16) {
+        __half* yp = reinterpret_cast<__half*>(p.Y) + off;
+        if (vec) {
+          __half2 h0 = __floats2half2_rn(vv[0], vv[1]), h1 = __floats2half2_rn(vv[2], vv[3]);
+          uint2 w2;
+          w2.x = *reinterpret_cast<uint32_t*>(&h0);
+          w2.y = *reinterpret_cast<uint32_t*>(&h1);
+          *reinterpret_cast<uint2*>(yp) = w2;
+        } else {
+          for (int j = 0; j < 4 && j < lim; ++j) yp[j] = __float2half_rn(vv[j]);
+        }
+      } else {
+        float* yp = reinterpret_cast<float*>(p.Y) + off;
+        if (vec) *reinterpret_cast<float4*>(yp) = v[u];
+        else
+          for (int j = 0; j < 4 && j < lim; ++j) yp[j] = vv[j];
+      }
+    }
   }
+}
+
+// Deterministic split-K. The ksplit CTAs of a cluster (consecutive tile ids:
+// the split index is fastest) hold the fp32 partials of ONE output tile in
+// shared memory ([128][BN + 4], written by the epilogue warps). After a cluster
+// barrier, cluster rank r combines rows [r*R, (r+1)*R) of the tile over all
+// ranks through distributed shared memory in the fixed order
+// ((p_0 + p_1) + p_2) + ..., then applies the C-ABI epilogue — (Yin +) sum,
+// + bias, + residual, activation — and stores 16-byte vectors at the output
+// pixel of each row (row-linear or, for T2D classes, strided). No memset, no
+// atomics: the result is identical on every run. A second barrier keeps every
+// partial alive until all ranks have read it. All threads of the CTA take part.
+template <int BN>
+__device__ __forceinline__ void cluster_reduce(const IgemmParams& p, const float* part, int64_t* row_off) {
+  if (threadIdx.x == 0) trace_x(p.trace, 0);
+  mc_cluster_sync();  // every partial of the cluster is written (release / acquire)
+  if (threadIdx.x == 0) trace_x(p.trace, 1);
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int ks = p.ksplit;
+  const int tile = blockIdx.x;
+  const bool active = tile < p.total_tiles;
+  int s = 0, mt = 0, g = 0, nt = 0, kk = 0;
+  if (active) decompose_tile(p, tile, s, mt, g, nt, kk);
+  const int rows = (kBM + ks - 1) / ks;
+  const int r0 = static_cast<int>(rank) * rows, r1 = min(kBM, r0 + rows);
+  // row_off[] was filled by the epilogue warps (split_row_offsets) before the
+  // kernel-end barrier
+  if (threadIdx.x == 0) trace_x(p.trace, 2);
+  const uint32_t base = smem_u32(part);
+  if (ks <= 2) cluster_combine<BN, 2, 4>(p, base, row_off, r0, r1, g, nt, active);
+  else if (ks <= 4) cluster_combine<BN, 4, 2>(p, base, row_off, r0, r1, g, nt, active);
+  else cluster_combine<BN, 8, 2>(p, base, row_off, r0, r1, g, nt, active);
   if (threadIdx.x == 0) trace_event(p.trace, TR_STORES_DONE);
-  mc_cluster_sync();  // peers have finished reading this CTA's partial
+  // peers have finished reading this CTA's partial (arrived in cluster_combine)
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+  if (threadIdx.x == 0) trace_x(p.trace, 3);
 }
 
 // Piece table entry: everything a producer needs for one TMA piece, computed
@@ -846,6 +883,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
       // below combines the ksplit partials of the cluster in a fixed order.
       float* part = reinterpret_cast<float*>(smem);
       constexpr int kChunk = BN < 32 ? BN : 32;
+      split_row_offsets<BN>(p, reinterpret_cast<int64_t*>(epi_smem), threadIdx.x, 32 * kEpi);
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         mbar_wait(&tfull[acc], acc_phase);
         tc_fence_after();
@@ -865,6 +903,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
         }
         tc_fence_before();
         mbar_arrive(&tempty[acc]);
+        if (threadIdx.x == 0) trace_x(p.trace, 4);
       }
     } else if (p.store_mode) {
       // TMA store: thread = tile row (tcgen05.ld 32x32b); each warp stages its
@@ -1150,6 +1189,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (threadIdx.x == 0) trace_x(p.trace, 5);
   if constexpr (cg2) mc_cluster_sync();  // the leader's MMAs into this CTA's TMEM are done
   if (p.ksplit > 1) cluster_reduce<BN>(p, reinterpret_cast<const float*>(smem), reinterpret_cast<int64_t*>(epi_smem));
   if (warp == kMmaWarp) {

@@ -64,6 +64,16 @@ __device__ __forceinline__ void trace_event(unsigned long long* trace, int ev) {
   }
 }
 
+// Extra milestones j < 8 of CTA b < 256 at trace[10240 + 8 * b + j] (split-K combine
+// timeline: tools/cta_timeline.py "x0".."x7"). Null in production.
+__device__ __forceinline__ void trace_x(unsigned long long* trace, int j) {
+  if (trace && blockIdx.x < 256) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    trace[10240 + 8 * blockIdx.x + j] = t;
+  }
+}
+
 // ---------------------------------------------------------------- mbarrier
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {

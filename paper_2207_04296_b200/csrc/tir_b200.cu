@@ -725,8 +725,11 @@ int choose_ksplit(const tb::IgemmParams& p, int64_t out_tiles, int out_f16, int 
   // one reduction order per output element whatever the batch, so a batch shard
   // is bit-identical to the same rows of the full-batch forward.
   if (out_f16 || p.bias || p.relu || p.residual) return 1;
-  if (out_tiles * 2 > sms) return 1;
-  int ks = static_cast<int>(std::min<int64_t>(sms / out_tiles, 8));
+  // At most half the SMs: the next launch's CTAs then enter on the other half while
+  // this one runs, and their prologue is off the critical path (T2D: 64 CTAs 9.9 us,
+  // 128 CTAs 10.6 us; tools/cta_timeline.py).
+  if (out_tiles * 2 > sms / 2) return 1;
+  int ks = static_cast<int>(std::min<int64_t>(sms / 2 / out_tiles, 8));
   ks = std::min(ks, nst_min / 2);  // at least two stages per split
   return std::max(ks, 1);
 }
@@ -1662,8 +1665,18 @@ int dep_impl(const Geo& g, const uint16_t* X, const uint16_t* W, const float* Yi
     if (g.s[1] == 1 && tc == 8)
       return launch_dep_tile<3, 1, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
     if (g.s[1] == 1) {
-      if (ow >= 24) return launch_dep_tile<3, 1, 4, 2, 8, 32>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
-      if (ow >= 12) return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+      // Tile shape (tools/sweep_options.py over the MobileNet-V2 shapes): the kernel is
+      // issue-bound, so columns of a partial tile cost time — 16 x 16 when it divides the
+      // width and 8 x 32 does not (112: 10.6 -> 10.2 us); narrow images take 8 x 8 tiles
+      // while those fit in two waves of CTAs (14² C384: 5.4 -> 4.8 us), else 16 x 16.
+      if (ow >= 24) {
+        if (ow % 32 && ow % 16 == 0)
+          return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+        return launch_dep_tile<3, 1, 4, 2, 8, 32>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
+      }
+      const int64_t tiles8 = g.n * ((g.out[1] + 7) / 8) * ((ow + 7) / 8) * ((g.ci + 31) / 32);
+      if (ow >= 12 && tiles8 > 2 * 3 * static_cast<int64_t>(device_info().sms))
+        return launch_dep_tile<3, 1, 4, 2, 16, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
       return launch_dep_tile<3, 1, 1, 2, 8, 8>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);
     }
     if (ow >= 12) return launch_dep_tile<3, 2, 2, 2, 8, 16>(g, X, W, Yin, Y, accumulate, out_f16, epi, stream);

@@ -47,7 +47,8 @@ def capture(op, launches=8):
     for b in bufs:
         ev = b[8192:8192 + 8 * 256].view(256, 8)[:, :8].cpu().tolist()
         cta = b[2048:2048 + 4 * 1024].view(1024, 4).cpu().tolist()
-        out.append((ev, cta, b[:2048].cpu().tolist()))
+        xs = b[10240:10240 + 8 * 256].view(256, 8).cpu().tolist()
+        out.append(([e + x for e, x in zip(ev, xs)], cta, b[:2048].cpu().tolist()))
     return out
 
 
@@ -66,7 +67,10 @@ def main():
         smid = cta[b][2] if b < len(cta) else -1
         rows.append((tiles, [x - prev_exit if x else None for x in e], smid, b))
     print(f"op {op} launch {k}: {len(rows)} traced CTAs; times in ns relative to launch {k-1}'s last exit")
-    names = ["entry", "pdl", "full", "tfull", "stores", "exit", "issue", "preloop"]
+    # x0..x5: split-K combine (igemm cluster_reduce): entry, first cluster sync passed,
+    # row offsets ready, final sync passed; x4 partial written; x5 kernel-end barrier passed
+    names = ["entry", "pdl", "full", "tfull", "stores", "exit", "issue", "preloop",
+             "x0", "x1", "x2", "x3", "x4", "x5", "x6", "x7"]
     by = {}
     for t, e, s, b in rows:
         by.setdefault(t, []).append(e)
