@@ -94,6 +94,11 @@ SMALL = {
     "DEP_c40_s2": tb.Conv("DEP", n=2, in_dhw=(1, 17, 17), ci=40, co=40, k=(1, 3, 3), s=(1, 2, 2), p=(0, 1, 1),
                           groups=40),
     "DEP_c12": tb.Conv("DEP", n=1, in_dhw=(1, 7, 7), ci=12, co=12, k=(1, 5, 5), p=(0, 2, 2), groups=12),
+    # tile shape by width (tir_b200.cu dep_impl): 112 wide takes 16 x 16 tiles; 14 wide with
+    # more 8 x 8 tiles than two waves of CTAs (16 x 2 x 2 x 18 > 888) takes 16 x 16 too
+    "DEP_w112": tb.Conv("DEP", n=2, in_dhw=(1, 112, 112), ci=32, co=32, k=(1, 3, 3), p=(0, 1, 1), groups=32),
+    "DEP_w14_many": tb.Conv("DEP", n=16, in_dhw=(1, 14, 14), ci=576, co=576, k=(1, 3, 3), p=(0, 1, 1),
+                            groups=576),
 }
 
 
