@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -1891,8 +1892,16 @@ int tir_b200_gmm_host(const uint16_t* A, const uint16_t* B, float* C, int64_t M,
   return TIR_B200_OK;
 }
 
+// debug (tools/e2e_probe.py): host microseconds of the last tir_b200_conv_host call —
+// [0] until every chunk is enqueued, [1] until the final synchronize returned
+static double g_host_times[2];
+void tir_b200_debug_host_times(double* out) {
+  out[0] = g_host_times[0];
+  out[1] = g_host_times[1];
+}
 int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const uint16_t* W,
                        float* Y, int accumulate) {
+  const auto t_entry = std::chrono::steady_clock::now();
   Geo g{};
   int rc = make_geo(desc, &g);
   if (rc) return rc;
@@ -1938,7 +1947,11 @@ int tir_b200_conv_host(const tir_b200_conv_desc* desc, const uint16_t* X, const 
     CUDA_TRY(cudaStreamWaitEvent(sd, t_host.ev[1 + kHostMaxChunks + c], 0));
     CUDA_TRY(cudaMemcpyAsync(Y + n0 * y_img, dy, (n1 - n0) * y_img * 4, cudaMemcpyDeviceToHost, sd));
   }
+  const auto t_enq = std::chrono::steady_clock::now();
   CUDA_TRY(cudaStreamSynchronize(sd));
+  const auto t_end = std::chrono::steady_clock::now();
+  g_host_times[0] = std::chrono::duration<double, std::micro>(t_enq - t_entry).count();
+  g_host_times[1] = std::chrono::duration<double, std::micro>(t_end - t_entry).count();
   return TIR_B200_OK;
 }
 
