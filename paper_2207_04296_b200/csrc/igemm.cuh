@@ -554,6 +554,36 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
   uint64_t t_start = 0;
   if (p.trace && threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
 
+  // Whole [b_res_rows, BN] resident panel of this CTA's (group, n-tile), once, issued
+  // by the EPILOGUE warps (idle until the first accumulator): a TMA issuer completes
+  // its requests one after another (~500 cycles each, tools/tmabw.cu), so panel boxes
+  // queued on the producers' threads would delay their first A stage.
+  auto issue_bres_panel = [&](int issuer, int nissuers) {
+    if (p.b_mode != B_RESIDENT || static_cast<int>(blockIdx.x) >= p.total_tiles) return;
+    constexpr int kBChunks = BN / Cfg::kBChunk;
+    int s0, mt0, g0, nt0;
+    decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
+    const int col0 = g0 * p.cog + nt0 * BN;
+    if (issuer == 0 && elect_one()) mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
+    __syncwarp();
+    if (elect_one()) {
+      if constexpr (GP) {
+        // one box of all b_res_rows rows per packed group's 32 columns
+        for (int ch = issuer; ch < kBChunks; ch += nissuers)
+          tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes, &p.tmB, bres_full,
+                      col0 + ch * Cfg::kBChunk, 0);
+      } else {
+        for (int r = issuer * Cfg::kBRows; r < p.b_res_rows; r += nissuers * Cfg::kBRows)
+#pragma unroll
+          for (int ch = 0; ch < kBChunks; ++ch)
+            tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
+                            static_cast<size_t>(r) * Cfg::kBRowBytes,
+                        &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
+      }
+    }
+    __syncwarp();
+  };
+
   if (warp >= kEpi && warp < kEpi + kProducers) {
     // ------------------------------------------------------------ producers
     // Every producer walks every stage and issues a round-robin share of its
@@ -646,31 +676,7 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     // the first TMA issues right after the preceding grid's memory is visible.
     pdl_wait();  // operands may be produced by the preceding kernel
     if (warp == kEpi && lane == 0) trace_event(p.trace, TR_PDL_DONE);
-    if (b_mode == B_RESIDENT && static_cast<int>(blockIdx.x) < p.total_tiles) {
-      // Whole [b_res_rows, BN] panel of this CTA's (group, n-tile), once.
-      int s0, mt0, g0, nt0;
-      decompose_tile(p, blockIdx.x, s0, mt0, g0, nt0);
-      const int col0 = g0 * p.cog + nt0 * BN;
-      if (pw == 0 && elect_one())
-        mbar_arrive_expect_tx(bres_full, static_cast<uint32_t>(p.b_res_rows) * BN * 2);
-      __syncwarp();
-      if (elect_one()) {
-        if constexpr (GP) {
-          // one box of all b_res_rows rows per packed group's 32 columns
-          for (int ch = pw; ch < kBChunks; ch += kProducers)
-            tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes, &p.tmB, bres_full,
-                        col0 + ch * Cfg::kBChunk, 0);
-        } else {
-          for (int r = pw * Cfg::kBRows; r < p.b_res_rows; r += kProducers * Cfg::kBRows)
-#pragma unroll
-            for (int ch = 0; ch < kBChunks; ++ch)
-              tma_load_2d(sB0 + static_cast<size_t>(ch) * p.b_res_rows * Cfg::kBRowBytes +
-                              static_cast<size_t>(r) * Cfg::kBRowBytes,
-                          &p.tmB, bres_full, col0 + ch * Cfg::kBChunk, r);
-        }
-      }
-      __syncwarp();
-    }
+    // (a resident B panel is issued by the epilogue warps: issue_bres_panel)
     uint32_t slot = 0, phase = 0;
     int it = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
@@ -871,7 +877,8 @@ __global__ void __launch_bounds__(IgemmCfg<BN, KS, EPI8>::kThreadsN, 1)
     }
   } else if (warp < kEpi) {
     // ------------------------------------------------------------ epilogue
-    pdl_wait();  // Y / Yin may be in use by the preceding kernel
+    pdl_wait();  // Y / Yin may be in use by the preceding kernel (and W by the panel load)
+    issue_bres_panel(static_cast<int>(warp), kEpi);
     const uint32_t q = warp & 3, hh = warp >> 2;
     constexpr int kHs = kEpi / 4;  // column chunks are dealt round-robin over the kHs warps of a quadrant
     uint8_t* wbuf = epi_smem + warp * Cfg::kEpiWarpBytes;
