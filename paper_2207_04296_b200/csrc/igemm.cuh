@@ -338,6 +338,7 @@ __device__ __forceinline__ void cluster_combine(const IgemmParams& p, uint32_t b
   const int passes = (items + per_pass - 1) / per_pass;  // CTA-uniform
   if (passes == 0) asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
   if (active) pdl_wait();  // Yin / residual may come from the preceding kernel
+  if (threadIdx.x == 0) trace_x(p.trace, 6);
 #pragma unroll 1
   for (int pass = 0; pass < passes; ++pass) {
     const int i0 = pass * per_pass + static_cast<int>(threadIdx.x);

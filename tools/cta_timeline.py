@@ -67,8 +67,9 @@ def main():
         smid = cta[b][2] if b < len(cta) else -1
         rows.append((tiles, [x - prev_exit if x else None for x in e], smid, b))
     print(f"op {op} launch {k}: {len(rows)} traced CTAs; times in ns relative to launch {k-1}'s last exit")
-    # x0..x5: split-K combine (igemm cluster_reduce): entry, first cluster sync passed,
-    # row offsets ready, final sync passed; x4 partial written; x5 kernel-end barrier passed
+    # x0..x7: split-K combine (igemm cluster_reduce): x0 entry, x1 first cluster sync passed,
+    # x2 tile coordinates read, x3 final sync passed; x4 partial written; x5 kernel-end
+    # barrier passed; x6 combine setup done (PDL wait passed); x7 last remote read consumed
     names = ["entry", "pdl", "full", "tfull", "stores", "exit", "issue", "preloop",
              "x0", "x1", "x2", "x3", "x4", "x5", "x6", "x7"]
     by = {}
